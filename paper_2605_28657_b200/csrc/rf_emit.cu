@@ -1,0 +1,236 @@
+// Admission init, emit statistics and deterministic squared-difference reductions
+// (SURVEY.md §8(a) A16, A17).
+#include <math.h>
+
+#include "rf_common.cuh"
+
+namespace rf {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedPerThread = 16;
+constexpr int kRedChunk = kRedThreads * kRedPerThread;  // elements per block
+constexpr int kMaxEmit = 16;
+constexpr int kMaxAdmit = 32;
+
+struct AdmitBatch {
+    int count;
+    rf_admit a[kMaxAdmit];
+};
+
+// _admit (pipeline.py:523-532): x = noise, or d*noise + (1-d)*source.
+__global__ void rf_admit_kernel(const __grid_constant__ AdmitBatch B, int64_t numel) {
+    const rf_admit &A = B.a[blockIdx.y];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double n = A.noise[i];
+        A.x[i] = A.source ? __dadd_rn(__dmul_rn(A.denoise, n), __dmul_rn(__dsub_rn(1.0, A.denoise), A.source[i]))
+                          : n;
+    }
+}
+
+// Fixed-shape reduction tree: thread-sequential over 16 elements, then a fixed
+// shuffle/shared tree.  The result depends only on numel, never on timing.
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < kRedThreads / 32; ++w) r = __dadd_rn(r, sh[w]);
+    }
+    __syncthreads();
+    return r;
+}
+
+struct EmitBatch {
+    int count;
+    rf_emit e[kMaxEmit];
+};
+
+// grid (chunks, emits): copy latent -> record, isfinite flag, chunk partials of
+// (lat - prev)^2 and (lat - ref)^2.
+__global__ void __launch_bounds__(kRedThreads)
+rf_emit_partials(const __grid_constant__ EmitBatch B, int64_t numel, const double *__restrict__ last,
+                 const double *__restrict__ ref, double *__restrict__ part_prev,
+                 double *__restrict__ part_ref, uint32_t *__restrict__ status) {
+    __shared__ double sh[kRedThreads / 32];
+    const int e = blockIdx.y;
+    const double *lat = B.e[e].latent;
+    double *rec = B.e[e].record;
+    const double *prev = e == 0 ? last : B.e[e - 1].latent;
+    const int64_t base = (int64_t)blockIdx.x * kRedChunk + (int64_t)threadIdx.x * kRedPerThread;
+    double sp = 0.0, sr = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kRedPerThread; ++k) {
+        int64_t i = base + k;
+        if (i < numel) {
+            double v = lat[i];
+            rec[i] = v;
+            if (!isfinite(v)) bad = true;
+            if (prev) {
+                double d = __dsub_rn(v, prev[i]);
+                sp = __dadd_rn(sp, __dmul_rn(d, d));
+            }
+            if (ref) {
+                double d = __dsub_rn(v, ref[i]);
+                sr = __dadd_rn(sr, __dmul_rn(d, d));
+            }
+        }
+    }
+    if (bad) atomicOr(status, RF_STATUS_NONFINITE);
+    double bp = block_sum(sp, sh);
+    double br = block_sum(sr, sh);
+    if (threadIdx.x == 0) {
+        part_prev[(int64_t)e * gridDim.x + blockIdx.x] = bp;
+        part_ref[(int64_t)e * gridDim.x + blockIdx.x] = br;
+    }
+}
+
+__global__ void rf_emit_finish(int count, int64_t chunks, int64_t numel, const double *part_prev,
+                               const double *part_ref, double *mse_prev, double *mse_ref, int has_last,
+                               int has_ref) {
+    const int e = threadIdx.x;
+    if (e >= count) return;
+    double sp = 0.0, sr = 0.0;
+    for (int64_t c = 0; c < chunks; ++c) {
+        sp = __dadd_rn(sp, part_prev[e * chunks + c]);
+        sr = __dadd_rn(sr, part_ref[e * chunks + c]);
+    }
+    // prev of emit 0 is `last` (may be absent); later emits always have a prev
+    mse_prev[e] = (e == 0 && !has_last) ? -1.0 : __ddiv_rn(sp, (double)numel);
+    mse_ref[e] = has_ref ? __ddiv_rn(sr, (double)numel) : -1.0;
+}
+
+}  // namespace rf
+
+using namespace rf;
+
+extern "C" int rf_admit_init(const rf_admit *admits, int count, int64_t numel, void *stream) {
+    if (count <= 0) return RF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int c0 = 0; c0 < count; c0 += kMaxAdmit) {
+        AdmitBatch B;
+        B.count = count - c0 < kMaxAdmit ? count - c0 : kMaxAdmit;
+        for (int i = 0; i < B.count; ++i) {
+            B.a[i] = admits[c0 + i];
+            if (!B.a[i].x || !B.a[i].noise) {
+                set_error("rf_admit_init: null pointer in admit %d", c0 + i);
+                return RF_EINVAL;
+            }
+        }
+        int64_t bx = (numel + 255) / 256;
+        if (bx > 1024) bx = 1024;
+        rf_admit_kernel<<<dim3((unsigned)bx, (unsigned)B.count), 256, 0, st>>>(B, numel);
+        RF_TRY_LAUNCH("rf_admit_kernel");
+    }
+    return RF_OK;
+}
+
+__global__ void rf_x0_kernel(double *out, const double *base, const double *hint, double hs,
+                             const double *timbre, double ts, const double *style, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double v = base[i];
+        if (hint) v = __dadd_rn(v, __dmul_rn(hs, hint[i]));
+        if (timbre) v = __dadd_rn(v, __dmul_rn(ts, timbre[i]));
+        if (style) v = __dadd_rn(v, style[i]);
+        out[i] = v;
+    }
+}
+
+extern "C" int rf_x0_compose(double *out, const double *base, const double *hint, double hs,
+                             const double *timbre, double ts, const double *style, int64_t numel,
+                             void *stream) {
+    if (!out || !base || numel <= 0) {
+        set_error("rf_x0_compose: bad arguments");
+        return RF_EINVAL;
+    }
+    int64_t bx = (numel + 255) / 256;
+    if (bx > 4096) bx = 4096;
+    rf_x0_kernel<<<(unsigned)bx, 256, 0, (cudaStream_t)stream>>>(out, base, hint, hs, timbre, ts, style,
+                                                                  numel);
+    RF_TRY_LAUNCH("rf_x0_kernel");
+    return RF_OK;
+}
+
+// Scratch for partials lives in a static device buffer grown on demand (tiny).
+static double *g_partials = nullptr;
+static int64_t g_partials_n = 0;
+
+static int ensure_partials(int64_t n) {
+    if (n <= g_partials_n) return RF_OK;
+    if (g_partials) cudaFree(g_partials);
+    g_partials = nullptr;
+    RF_TRY_CUDA(cudaMalloc(&g_partials, n * sizeof(double)));
+    g_partials_n = n;
+    return RF_OK;
+}
+
+extern "C" int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, const double *last,
+                             const double *reference, double *mse_prev, double *mse_ref,
+                             uint32_t *status, void *stream) {
+    if (count <= 0) return RF_OK;
+    if (count > kMaxEmit || !emits || !mse_prev || !mse_ref || !status || numel <= 0) {
+        set_error("rf_emit_stats: bad arguments (count %d)", count);
+        return RF_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    EmitBatch B;
+    B.count = count;
+    for (int i = 0; i < count; ++i) B.e[i] = emits[i];
+    int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
+    int rc = ensure_partials(2 * chunks * count);
+    if (rc) return rc;
+    double *pp = g_partials, *pr = g_partials + chunks * count;
+    rf_emit_partials<<<dim3((unsigned)chunks, (unsigned)count), kRedThreads, 0, st>>>(
+        B, numel, last, reference, pp, pr, status);
+    RF_TRY_LAUNCH("rf_emit_partials");
+    rf_emit_finish<<<1, 32, 0, st>>>(count, chunks, numel, pp, pr, mse_prev, mse_ref, last != nullptr,
+                                     reference != nullptr);
+    RF_TRY_LAUNCH("rf_emit_finish");
+    return RF_OK;
+}
+
+// mse of two arrays with the same fixed-order tree (used by the Python seams).
+__global__ void __launch_bounds__(kRedThreads)
+rf_sqdiff_partials(const double *__restrict__ a, const double *__restrict__ b, int64_t numel,
+                   double *__restrict__ part) {
+    __shared__ double sh[kRedThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kRedChunk + (int64_t)threadIdx.x * kRedPerThread;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRedPerThread; ++k) {
+        int64_t i = base + k;
+        if (i < numel) {
+            double d = __dsub_rn(a[i], b[i]);
+            s = __dadd_rn(s, __dmul_rn(d, d));
+        }
+    }
+    double r = block_sum(s, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+__global__ void rf_sum_finish(const double *part, int64_t chunks, int64_t numel, double *out) {
+    double s = 0.0;
+    for (int64_t c = 0; c < chunks; ++c) s = __dadd_rn(s, part[c]);
+    *out = __ddiv_rn(s, (double)numel);
+}
+
+extern "C" int rf_mse(const double *a, const double *b, int64_t numel, double *out, void *stream) {
+    if (!a || !b || !out || numel <= 0) {
+        set_error("rf_mse: bad arguments");
+        return RF_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
+    int rc = ensure_partials(chunks);
+    if (rc) return rc;
+    rf_sqdiff_partials<<<(unsigned)chunks, kRedThreads, 0, st>>>(a, b, numel, g_partials);
+    RF_TRY_LAUNCH("rf_sqdiff_partials");
+    rf_sum_finish<<<1, 1, 0, st>>>(g_partials, chunks, numel, out);
+    RF_TRY_LAUNCH("rf_sum_finish");
+    return RF_OK;
+}

@@ -1,0 +1,299 @@
+// Fused per-tick solver: toy velocity + condition blend + guidance + SDE/ODE update
+// for every active ring row in one launch.
+//
+// Reference semantics, in the reference's floating-point operation order:
+//   ToyFlowModel.velocity     model.py:133-152   v = (x - x0)/t + (jitter*t)*n_model
+//   x0_of                     model.py:123-131   x0 = partial(prompt,hint,timbre) + style_offset
+//   blend_conditions          solver.py:204-227  v = (sum w_i v_i) / (sum w_i)
+//   guided_velocity           solver.py:141-201  CFG / RCFG / APG momentum / rescale
+//   _morph_target             solver.py:230-238
+//   sde_step                  solver.py:273-306
+//   ode_step                  solver.py:241-270
+// Every floating-point operation uses an explicit round-to-nearest intrinsic
+// (__dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn) so nvcc cannot contract to FMA: numpy
+// evaluates one ufunc per operation, so this reproduces its results bit for bit.
+//
+// Layout: latents [T, D] frame-major float64.  A group of `lpf` lanes owns one frame
+// (lpf = D/2 rounded up to a power of two, <= 32), each lane two adjacent channels
+// (16-byte loads), so a D=64 frame is one fully coalesced 512-byte warp access per
+// operand; the cfg-rescale norms are in-register shuffles over the group.
+#include "rf_common.cuh"
+
+namespace rf {
+
+constexpr int kTickMaxRows = 32;
+constexpr int kTickMaxGroups = 4;  // channel groups of 64 per lane -> D <= 256
+
+struct TickBatch {
+    int count;
+    rf_row rows[kTickMaxRows];
+};
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ double curve_or(const double *c, int64_t f, double dflt) {
+    return c ? c[f] : dflt;
+}
+
+// One element of the fused step; returns the new x and the guided output (for the
+// rescale pass the caller needs the pre-rescale `out` and `vc`).
+struct ElemVel {
+    double vc;   // positive (blended) velocity
+    double out;  // guided velocity before rescale
+};
+
+__device__ __forceinline__ double toy_velocity(double x, double x0p, double style, double t,
+                                               const double *nm, double jt, int64_t i) {
+    double x0 = dadd(x0p, style);
+    double v = ddiv(dsub(x, x0), t);
+    if (nm) v = dadd(v, dmul(jt, nm[i]));
+    return v;
+}
+
+__device__ __forceinline__ ElemVel velocity_elem(const rf_row &R, const double *__restrict__ style,
+                                                 double x, int64_t f, int64_t i) {
+    const double t = R.t_curr;
+    const bool cond_v = (R.flags & RF_ROWF_COND_V) != 0;
+    double v;
+    if (R.n_cond == 1) {
+        v = cond_v ? R.cond_x0[0][i]
+                   : toy_velocity(x, R.cond_x0[0][i], style[i], t, R.noise_model, R.jitter_t, i);
+    } else {
+        double acc = 0.0, tot = 0.0;
+        for (int k = 0; k < R.n_cond; ++k) {
+            double vk = cond_v ? R.cond_x0[k][i]
+                               : toy_velocity(x, R.cond_x0[k][i], style[i], t, R.noise_model,
+                                              R.jitter_t, i);
+            double w = curve_or(R.cond_w[k], f, 1.0);
+            acc = dadd(acc, dmul(w, vk));
+            tot = dadd(tot, w);
+        }
+        v = ddiv(acc, tot);
+    }
+    ElemVel ev;
+    ev.vc = v;
+    ev.out = v;
+    if (R.neg_kind == RF_NEG_NONE) return ev;
+    double neg;
+    if (R.neg_kind == RF_NEG_UNCOND) {
+        double vu = (R.flags & RF_ROWF_UNCOND_V)
+                        ? R.uncond_x0[i]
+                        : toy_velocity(x, R.uncond_x0[i], style[i], t, R.noise_model, R.jitter_t, i);
+        if (R.flags & RF_ROWF_WRITE_RESIDUAL) {
+            double res = dsub(v, vu);
+            R.residual[i] = res;
+            neg = dsub(v, res);
+        } else {
+            neg = vu;
+        }
+    } else if (R.neg_kind == RF_NEG_RESIDUAL) {
+        neg = dsub(v, R.residual[i]);
+    } else {  // RF_NEG_PREV
+        neg = R.prev_positive[i];
+    }
+    if (R.flags & RF_ROWF_WRITE_PREV) R.prev_positive[i] = v;
+    double delta = dsub(v, neg);
+    const double *apg = R.curves[RF_CURVE_APG];
+    if (apg) {
+        double m = (R.flags & RF_ROWF_MOMENTUM_INIT) ? 0.0 : R.momentum[i];
+        m = dadd(dmul(apg[f], m), delta);
+        R.momentum[i] = m;
+        delta = m;
+    }
+    double scale = curve_or(R.curves[RF_CURVE_GUIDANCE], f, 1.0);
+    ev.out = dadd(v, dmul(dsub(scale, 1.0), delta));
+    return ev;
+}
+
+__device__ __forceinline__ double morph(const rf_row &R, double x0p, int64_t f, int64_t i) {
+    double a = curve_or(R.curves[RF_CURVE_X0_STRENGTH], f, 1.0);
+    return dadd(dmul(dsub(1.0, a), x0p), dmul(a, R.x0_target[i]));
+}
+
+__device__ __forceinline__ double solve_elem(const rf_row &R, double x, double v, int64_t f,
+                                             int64_t i) {
+    const double tc = R.t_curr, tn = R.t_next;
+    if (R.solver == RF_SOLVER_SDE) {
+        double x0p = dsub(x, dmul(v, tc));
+        if (R.x0_target) x0p = morph(R, x0p, f, i);
+        double n = R.noise_step[i];
+        double tnn = dmul(tn, n);
+        double omt = dsub(1.0, tn);
+        double full = dadd(tnn, dmul(omt, x0p));
+        if (!R.source) return full;
+        double c = curve_or(R.curves[RF_CURVE_SDE], f, 1.0);
+        double src = dadd(tnn, dmul(omt, R.source[i]));
+        return dadd(dmul(c, full), dmul(dsub(1.0, c), src));
+    }
+    // ODE
+    if (R.flags & RF_ROWF_ODE_MORPH) {
+        double x0p = dsub(x, dmul(v, tc));
+        v = ddiv(dsub(x, morph(R, x0p, f, i)), tc);
+    }
+    const double *vs = R.curves[RF_CURVE_VSCALE];
+    if (vs) v = dmul(vs[f], v);
+    double xn = dadd(x, dmul(v, dsub(tn, tc)));
+    if (R.noise_step) xn = dadd(xn, dmul(R.curves[RF_CURVE_ODE_NOISE][f], R.noise_step[i]));
+    return xn;
+}
+
+// Sum of squares over one frame's channels.  numpy's np.linalg.norm(axis=1) reduces
+// each row with pairwise summation; here the order is a fixed shuffle tree, so the
+// rescale factor is deterministic but may differ from numpy in the last ulp.
+template <int LPF>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int off = LPF / 2; off > 0; off >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+
+template <int LPF>
+__global__ void __launch_bounds__(256)
+rf_tick_kernel(const __grid_constant__ TickBatch B, int64_t T, int64_t D, const double *__restrict__ style) {
+    const rf_row &R = B.rows[blockIdx.y];
+    const int lane = threadIdx.x & 31;
+    constexpr int FPW = 32 / LPF;  // frames per warp step
+    const int sub = lane / LPF, gl = lane % LPF;
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const bool rescale = R.neg_kind != RF_NEG_NONE && R.curves[RF_CURVE_RESCALE] != nullptr;
+
+    for (int64_t f0 = wid * FPW; f0 < T; f0 += warps_total * FPW) {
+        const int64_t f = f0 + sub;
+        const bool live = f < T;
+        double vcs[kTickMaxGroups][2], outs[kTickMaxGroups][2], xs[kTickMaxGroups][2];
+        double ss_out = 0.0, ss_pos = 0.0;
+#pragma unroll
+        for (int g = 0; g < kTickMaxGroups; ++g) {
+            const int64_t c = (int64_t)g * 2 * LPF + 2 * gl;
+            if (!live || c >= D) continue;
+            const int64_t i = f * D + c;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (c + e >= D) continue;
+                double x = R.x ? R.x[i + e] : 0.0;
+                ElemVel ev = velocity_elem(R, style, x, f, i + e);
+                xs[g][e] = x;
+                vcs[g][e] = ev.vc;
+                outs[g][e] = ev.out;
+                if (rescale) {
+                    ss_out = dadd(ss_out, dmul(ev.out, ev.out));
+                    ss_pos = dadd(ss_pos, dmul(ev.vc, ev.vc));
+                }
+            }
+        }
+        double factor = 1.0;
+        if (rescale) {
+            ss_out = group_sum<LPF>(ss_out);
+            ss_pos = group_sum<LPF>(ss_pos);
+            if (live) {
+                double no = sqrt(ss_out), np_ = sqrt(ss_pos);
+                double keep = R.curves[RF_CURVE_RESCALE][f];
+                double blended = dadd(dmul(keep, no), dmul(dsub(1.0, keep), np_));
+                factor = no > 0.0 ? ddiv(blended, no) : 1.0;
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < kTickMaxGroups; ++g) {
+            const int64_t c = (int64_t)g * 2 * LPF + 2 * gl;
+            if (!live || c >= D) continue;
+            const int64_t i = f * D + c;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (c + e >= D) continue;
+                double v = rescale ? dmul(outs[g][e], factor) : outs[g][e];
+                if (R.v_out) R.v_out[i + e] = v;
+                if (!(R.flags & RF_ROWF_NO_STEP)) R.x[i + e] = solve_elem(R, xs[g][e], v, f, i + e);
+            }
+        }
+    }
+}
+
+template <int LPF>
+static int launch_tick(const TickBatch &B, int64_t T, int64_t D, const double *style,
+                       cudaStream_t st) {
+    constexpr int FPW = 32 / LPF;
+    const int warps_per_block = 8;
+    int64_t frames_per_block = (int64_t)warps_per_block * FPW;
+    int64_t bx = (T + frames_per_block - 1) / frames_per_block;
+    // keep >= ~2 waves over the SMs across all rows without oversubscribing tiny rows
+    if (bx < 1) bx = 1;
+    dim3 grid((unsigned)bx, (unsigned)B.count);
+    rf_tick_kernel<LPF><<<grid, warps_per_block * 32, 0, st>>>(B, T, D, style);
+    RF_TRY_LAUNCH("rf_tick_kernel");
+    return RF_OK;
+}
+
+}  // namespace rf
+
+using namespace rf;
+
+extern "C" int rf_tick_solve(const rf_row *rows, int count, int64_t frames, int64_t channels,
+                             const double *style_offset, void *stream) {
+    if (count <= 0) return RF_OK;
+    if (!rows || !style_offset || frames <= 0 || channels <= 0) {
+        set_error("rf_tick_solve: bad arguments");
+        return RF_EINVAL;
+    }
+    if (channels > 2 * 32 * kTickMaxGroups) {
+        set_error("rf_tick_solve: channels %lld > %d", (long long)channels, 2 * 32 * kTickMaxGroups);
+        return RF_EINVAL;
+    }
+    for (int r = 0; r < count; ++r) {
+        const rf_row &R = rows[r];
+        const bool velocity_only = (R.flags & RF_ROWF_NO_STEP) != 0;
+        if ((!R.x && !velocity_only) || (velocity_only && !R.v_out) || R.n_cond < 1 ||
+            R.n_cond > RF_MAX_COND || (!(R.t_curr > 0.0) && !(R.flags & RF_ROWF_COND_V))) {
+            set_error("rf_tick_solve: bad row %d", r);
+            return RF_EINVAL;
+        }
+        for (int k = 0; k < R.n_cond; ++k)
+            if (!R.cond_x0[k]) {
+                set_error("rf_tick_solve: row %d missing cond_x0[%d]", r, k);
+                return RF_EINVAL;
+            }
+        if (!velocity_only && R.solver == RF_SOLVER_SDE && !R.noise_step) {
+            set_error("rf_tick_solve: row %d sde without noise", r);
+            return RF_EINVAL;
+        }
+        if (R.solver == RF_SOLVER_ODE && R.noise_step && !R.curves[RF_CURVE_ODE_NOISE]) {
+            set_error("rf_tick_solve: row %d ode noise without curve", r);
+            return RF_EINVAL;
+        }
+        if (!(R.flags & RF_ROWF_COND_V) && !R.x) {
+            set_error("rf_tick_solve: row %d toy velocity needs x", r);
+            return RF_EINVAL;
+        }
+        if (R.neg_kind == RF_NEG_UNCOND && !R.uncond_x0) {
+            set_error("rf_tick_solve: row %d guidance without uncond_x0", r);
+            return RF_EINVAL;
+        }
+        if (R.curves[RF_CURVE_APG] && R.neg_kind != RF_NEG_NONE && !R.momentum) {
+            set_error("rf_tick_solve: row %d apg without momentum buffer", r);
+            return RF_EINVAL;
+        }
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t half = (channels + 1) / 2;
+    int lpf = 1;
+    while (lpf < half && lpf < 32) lpf <<= 1;
+    for (int r0 = 0; r0 < count; r0 += kTickMaxRows) {
+        TickBatch B;
+        B.count = count - r0 < kTickMaxRows ? count - r0 : kTickMaxRows;
+        for (int r = 0; r < B.count; ++r) B.rows[r] = rows[r0 + r];
+        int rc;
+        switch (lpf) {
+            case 1: rc = launch_tick<1>(B, frames, channels, style_offset, st); break;
+            case 2: rc = launch_tick<2>(B, frames, channels, style_offset, st); break;
+            case 4: rc = launch_tick<4>(B, frames, channels, style_offset, st); break;
+            case 8: rc = launch_tick<8>(B, frames, channels, style_offset, st); break;
+            case 16: rc = launch_tick<16>(B, frames, channels, style_offset, st); break;
+            default: rc = launch_tick<32>(B, frames, channels, style_offset, st); break;
+        }
+        if (rc) return rc;
+    }
+    return RF_OK;
+}
