@@ -22,6 +22,7 @@
 // ~1e-12 per position) cannot be represented by the 16-state tables; pass 1 flags
 // its draw and pass 2 resolves that draw with a sequential walk instead.
 #include <math.h>
+#include <math_constants.h>
 
 #include "rf_common.cuh"
 #include "rf_zig_tables.h"
@@ -78,6 +79,92 @@ __device__ __forceinline__ void load_zig(ZigSmem &z) {
     }
 }
 
+// log1p exactly as the reference's numpy computes it on this image's x86-64 hosts:
+// numpy's npy_log1p is glibc 2.39's log1p, which the ifunc resolver dispatches to
+// __log1p_fma on FMA/AVX2 CPUs -- the fdlibm algorithm (sysdeps/ieee754/dbl-64/
+// s_log1p.c) compiled with FMA contraction.  The operation sequence below follows
+// that object code (decoded from libm.so.6) one IEEE operation at a time, so the
+// tail-path values of the ziggurat are bit-identical to numpy's.  CUDA's own log1p
+// differs in the last ulp for ~0.5% of arguments.
+__device__ __noinline__ double glibc_log1p_fma(double x) {
+    const double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2, Lp3 = 0x1.2492494229359p-2;
+    const double Lp4 = 0x1.c71c51d8e78afp-3, Lp5 = 0x1.7466496cb03dep-3, Lp6 = 0x1.39a09d078c69fp-3;
+    const double Lp7 = 0x1.2f112df3e5244p-3;
+    const double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+    const int hx = __double2hiint(x);
+    const unsigned ax = (unsigned)hx & 0x7fffffffu;
+    int k;
+    double f, c = 0.0, u;
+    unsigned hu;
+    bool poly_k0 = false;
+    if (hx <= 0x3fda8279) {                       // x < 0.41422 (all negatives too)
+        if (ax > 0x3fefffffu) {                   // x <= -1
+            if (x == -1.0) return -CUDART_INF;
+            return CUDART_NAN;
+        }
+        if (ax <= 0x3e1fffffu) {                  // |x| < 2^-29
+            if (ax > 0x3c8fffffu) return __fma_rn(-__dmul_rn(x, x), 0.5, x);
+            return x;
+        }
+        if ((unsigned)hx + 0x402d413cu > 0x402d413cu) {  // -0.2929 < x < 0.41422: k = 0, f = x
+            k = 0;
+            f = x;
+            hu = 1;
+            poly_k0 = true;
+        }
+    } else if (hx > 0x7fefffff) {
+        return __dadd_rn(x, x);
+    }
+    if (!poly_k0) {
+        if (hx > 0x433fffff) {                    // x >= 2^53
+            k = (hx >> 20) - 1023;
+            u = x;
+            c = 0.0;
+            hu = (unsigned)hx;
+        } else {
+            u = __dadd_rn(x, 1.0);
+            hu = (unsigned)__double2hiint(u);
+            k = (int)(hu >> 20) - 1023;
+            c = (k > 0) ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+            c = __ddiv_rn(c, u);
+        }
+        hu &= 0x000fffffu;
+        if (hu > 0x6a09du) {
+            k += 1;
+            u = __hiloint2double((int)(hu | 0x3fe00000u), __double2loint(u));
+            hu = (0x00100000u - hu) >> 2;
+        } else {
+            u = __hiloint2double((int)(hu | 0x3ff00000u), __double2loint(u));
+        }
+        f = __dsub_rn(u, 1.0);
+    }
+    const double hfsq = __dmul_rn(__dmul_rn(f, 0.5), f);
+    if (hu == 0) {                                // |f| < 2^-20
+        if (f == 0.0) {
+            if (k == 0) return 0.0;
+            const double kd = (double)k;
+            return __fma_rn(kd, ln2_hi, __fma_rn(kd, ln2_lo, c));
+        }
+        const double R = __dmul_rn(__fma_rn(-f, 0x1.5555555555555p-1, 1.0), hfsq);
+        if (k == 0) return __dsub_rn(f, R);
+        const double kd = (double)k;
+        const double t = __dsub_rn(__dsub_rn(R, __fma_rn(kd, ln2_lo, c)), f);
+        return __fma_rn(kd, ln2_hi, -t);
+    }
+    const double s = __ddiv_rn(f, __dadd_rn(f, 2.0));
+    const double z = __dmul_rn(s, s);
+    const double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+    const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+    double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+    R = __fma_rn(z4, R3, R);
+    R = __fma_rn(z6, R4, R);
+    const double w = __dmul_rn(__dadd_rn(R, hfsq), s);
+    if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, w));
+    const double kd = (double)k;
+    const double t = __dsub_rn(__dsub_rn(hfsq, __dadd_rn(__fma_rn(kd, ln2_lo, c), w)), f);
+    return __fma_rn(kd, ln2_hi, -t);
+}
+
 // A full draw starting at stream position p (numpy random_standard_normal, every
 // branch).  Used for the 1-2% of positions that miss the fast path.
 __device__ __noinline__ void zig_slow(uint64_t k0, uint64_t k1, uint64_t p, const ZigSmem &z,
@@ -102,8 +189,8 @@ __device__ __noinline__ void zig_slow(uint64_t k0, uint64_t k1, uint64_t p, cons
                 double u1 = u64_to_unit_double(philox_word(k0, k1, q2));
                 double u2 = u64_to_unit_double(philox_word(k0, k1, q2 + 1));
                 q2 += 2;
-                double xx = __dmul_rn(-RF_ZIG_NOR_INV_R, log1p(-u1));
-                double yy = -log1p(-u2);
+                double xx = __dmul_rn(-RF_ZIG_NOR_INV_R, glibc_log1p_fma(-u1));
+                double yy = -glibc_log1p_fma(-u2);
                 if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
                     *len_out = (uint32_t)(q2 - p);
                     double m = __dadd_rn(RF_ZIG_NOR_R, xx);

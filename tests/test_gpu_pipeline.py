@@ -104,13 +104,14 @@ def test_backpressure_and_errors(rf):
     T, D = 32, 4
     pipe = rf.StreamPipeline(rf.PipelineConfig(depth=2, steps=4, frames=T, channels=D, auto_submit=False),
                              request=rf.GenerationRequest(conditions=(rf.ConditionSet(1),)))
+    pipe.set_denoise(0.5)
+    with pytest.raises(ValueError):   # denoise < 1 needs a source
+        pipe.submit(rf.GenerationRequest(conditions=(rf.ConditionSet(2),)))
+    pipe.set_denoise(1.0)
     pipe.submit()
     pipe.submit()
     with pytest.raises(rf.BackpressureError):
         pipe.submit()
-    pipe.set_denoise(0.5)
-    with pytest.raises(ValueError):
-        pipe.submit(rf.GenerationRequest(conditions=(rf.ConditionSet(2),)))
     with pytest.raises(KeyError):
         pipe.set_shared_curve("nope", 1.0)
     with pytest.raises(ValueError):
