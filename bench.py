@@ -80,9 +80,18 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            # one synchronous sample at the end so a short timed region still has data
+            try:
+                snap = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                      timeout=20).stdout
+            except Exception:
+                snap = ""
             self.proc.terminate()
             self.proc.wait()
             self.fh.close()
+            with open(self.path, "a") as fh:
+                fh.write(snap)
 
     def summary(self):
         if self.proc is None:

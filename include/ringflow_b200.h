@@ -159,8 +159,10 @@ int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, const double *
 /* ------------------------------------------------------------- codec (B1-B9) -----
  * ToyCodec (codec.py:67-174).  The decode of an extended window [F, C] runs the
  * dilated conv stack (tanh, valid-row mask), the per-frame upsampler and
- * quantize_pcm in one kernel, writing only the trimmed samples.
- *   latent: device [frames, C]; kernels: device [L, 3, C, C]; upsample: device [hop, C]
+ * quantize_pcm in one clustered kernel, writing only the trimmed samples.
+ *   latent: device [frames, C]; kernels: device [L, 3, C, C];
+ *   upsample_t: device [C, hop] (the reference's [hop, C] upsampler, transposed);
+ *   C must be a multiple of 8 and <= 64.
  *   window [start, stop) and overlap as in windowed_decode (codec.py:136-164);
  *   full_decode is the window [0, frames) with overlap 0 and no mask.
  *   out: device int16 [(stop - start) * hop].
@@ -170,7 +172,7 @@ int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, const double *
 int64_t rf_decode_workspace_bytes(int64_t out_frames, int64_t channels);
 int rf_decode_window(const double *latent, int64_t frames, int64_t channels,
                      const double *kernels, const int32_t *dilations, int32_t n_layers,
-                     const double *upsample, int64_t hop, int64_t start, int64_t stop,
+                     const double *upsample_t, int64_t hop, int64_t start, int64_t stop,
                      int64_t overlap, int32_t full, int16_t *out, void *workspace,
                      int64_t workspace_bytes, void *stream);
 

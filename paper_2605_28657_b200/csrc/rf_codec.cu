@@ -1,92 +1,52 @@
-// Windowed / full toy-codec decode (reference codec.py:93-164).
+// Windowed / full toy-codec decode in ONE launch (reference
+// codec.py:93-164).
 //
-// Two kernels:
-//   rf_conv_stack   : for each trimmed output frame, the dilated conv stack
-//                     (kernel 3, tanh, zero outside the valid range) evaluated on a
-//                     halo-staged shared-memory tile -> h[F_out, C] (float64).
-//   rf_upsample_q16 : the per-frame linear upsampler h @ U^T as a register-tiled GEMM
-//                     (M = output frames, N = hop, K = C) with quantize_pcm fused in
-//                     the epilogue -> int16 samples.
-// Every layer value at global frame g is a fixed-order sum over (tap 0,1,2) x (input
-// channel 0..C-1) of values that are zero outside [vlo, vhi) -- the same in the full
-// and the windowed decode -- so windowed == full holds bit for bit on the GPU whenever
+// Layout: a thread-block cluster of NC (= 8) CTAs owns a tile of TF output frames.
+//   * Every CTA stages the tile's input frames plus the receptive-field halo
+//     [g0 - rf, g0 + TF + rf) for all C channels in shared memory (zero outside the
+//     valid range [vlo, vhi), exactly the zeros the reference's padding/mask produce).
+//   * Layer l: CTA r computes output channels [r*C/NC, (r+1)*C/NC) for the frames whose
+//     taps stay inside the staged region (the region shrinks by d_l per side), with
+//     its slice of the conv weights resident in shared memory.  Each output is a
+//     fixed-order sum (4 lanes x C/4 input channels x 3 taps, fixed shuffle tree), tanh,
+//     and zero outside [vlo, vhi).
+//   * After each layer the cluster synchronises and every CTA gathers the other CTAs'
+//     channel slices through distributed shared memory (DSMEM), so activations never
+//     leave the SMs.
+//   * Finally CTA r computes samples [r*hop/NC, (r+1)*hop/NC) of every tile frame:
+//     pcm[f][j] = quantize(sum_c h[f][c] * U[j][c]), with U^T streamed from L2 and the
+//     int16 rounding/clipping of quantize_pcm (codec.py:27-31) fused.
+// Because every value at global frame g is computed by the same fixed-order arithmetic
+// whatever the window, windowed == full holds bit for bit on the GPU whenever
 // overlap >= receptive field (the reference's contract, codec.py:1-11).
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include "rf_common.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace rf {
 
-constexpr int kConvThreads = 256;
-constexpr int kConvTile = 16;  // output frames per CTA
+constexpr int kNC = 8;          // CTAs per cluster
+constexpr int kTF = 16;         // output frames per cluster
+constexpr int kThreads = 256;
+constexpr int kKS = 8;          // lanes cooperating on one conv output
 constexpr int kMaxC = 64;
 
-struct ConvArgs {
-    const double *latent;
-    int64_t frames, C;
-    const double *kernels;  // [L,3,C,C] (tap, in k, out c)
+struct DecodeArgs {
+    const double *latent;       // [frames, C]
+    int64_t frames;
+    int C, CS;                  // channels, channels per CTA (informational)
+    const double *kernels;      // [L,3,C,C] (tap, in k, out c)
     int32_t dil[RF_MAX_CODEC_LAYERS];
-    int32_t L, rf;          // rf = sum of dilations
-    int64_t vlo, vhi;       // valid global frame range
-    int64_t start, nout;    // trimmed output frames [start, start+nout)
-    double *h;              // [nout, C]
+    int32_t L, rf;
+    int64_t vlo, vhi;           // valid global frame range
+    int64_t start, nout;        // output frames [start, start + nout)
+    const double *upT;          // [C, hop] (transposed upsampler)
+    int64_t hop;
+    int16_t *out;               // [nout * hop]
 };
-
-// Shared tile covers global frames [g0 - rf, g0 + kConvTile + rf).
-__global__ void __launch_bounds__(kConvThreads)
-rf_conv_stack(const __grid_constant__ ConvArgs A) {
-    extern __shared__ double sm[];
-    const int C = (int)A.C;
-    const int W = kConvTile + 2 * A.rf;  // tile width in frames
-    double *buf0 = sm, *buf1 = sm + (int64_t)W * C;
-    const int64_t g0 = A.start + (int64_t)blockIdx.x * kConvTile;
-    const int64_t gbase = g0 - A.rf;
-    for (int idx = threadIdx.x; idx < W * C; idx += blockDim.x) {
-        int w = idx / C, c = idx % C;
-        int64_t g = gbase + w;
-        buf0[idx] = (g >= A.vlo && g < A.vhi) ? A.latent[g * C + c] : 0.0;
-    }
-    __syncthreads();
-    // layer l valid computed region shrinks by the remaining dilations
-    int lo = 0, hi = W;  // region of buf holding correct values for the current layer input
-    double *in = buf0, *out = buf1;
-    for (int l = 0; l < A.L; ++l) {
-        const int d = A.dil[l];
-        const int olo = lo + d, ohi = hi - d;  // frames whose taps stay inside [lo, hi)
-        const double *K = A.kernels + (int64_t)l * 3 * C * C;
-        const int n = (ohi - olo) * C;
-        for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
-            const int w = olo + idx / C, c = idx % C;
-            const int64_t g = gbase + w;
-            double acc = 0.0;
-            if (g >= A.vlo && g < A.vhi) {
-                double tap_sum[3];
-#pragma unroll
-                for (int tap = 0; tap < 3; ++tap) {
-                    const double *row = in + (int64_t)(w + (tap - 1) * d) * C;
-                    const double *kk = K + (int64_t)tap * C * C + c;
-                    double s = 0.0;
-                    for (int k = 0; k < C; ++k) s = fma(row[k], kk[(int64_t)k * C], s);
-                    tap_sum[tap] = s;
-                }
-                acc = tanh((tap_sum[0] + tap_sum[1]) + tap_sum[2]);
-            }
-            out[w * C + c] = acc;
-        }
-        __syncthreads();
-        lo = olo;
-        hi = ohi;
-        double *t = in;
-        in = out;
-        out = t;
-    }
-    // lo..hi now equals [rf, rf + kConvTile)
-    for (int idx = threadIdx.x; idx < kConvTile * C; idx += blockDim.x) {
-        const int w = idx / C, c = idx % C;
-        const int64_t o = (int64_t)blockIdx.x * kConvTile + w;
-        if (o < A.nout) A.h[o * C + c] = in[(A.rf + w) * C + c];
-    }
-}
 
 // quantize_pcm (codec.py:27-31): copysign(floor(|32767 s| + 0.5), s), clip, int16.
 __device__ __forceinline__ int16_t quantize_pcm(double s) {
@@ -96,52 +56,151 @@ __device__ __forceinline__ int16_t quantize_pcm(double s) {
     return (int16_t)(int)r;
 }
 
-constexpr int kUpTM = 32, kUpTN = 128, kUpThreads = 256;
-// each thread: 4 frames x 4 samples
+template <int C>
+__global__ void __launch_bounds__(kThreads)
+rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
+    constexpr int CS = C / kNC;       // output channels per CTA
+    constexpr int KPER = C / kKS;     // input channels per lane of a conv output
+    extern __shared__ __align__(16) double sm[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int L = A.L;
+    const int W = kTF + 2 * A.rf;
+    const int jper = (int)((A.hop + kNC - 1) / kNC);
+    double *act = sm;                                   // [W][C]   current layer input
+    double *part0 = act + (size_t)W * C;                // [2][W][CS] this CTA's layer output
+    double *wts = part0 + (size_t)2 * W * CS;           // [L][3][C][CS]
+    double *hT = wts + (size_t)L * 3 * C * CS;          // [C][kTF] final layer, transposed
+    double *ups = hT + (size_t)C * kTF;                 // [C][jper] this CTA's U^T slice
+    const int64_t tile = blockIdx.x / kNC;
+    const int64_t g0 = A.start + tile * kTF;
+    const int64_t gbase = g0 - A.rf;
+    const int c0 = rank * CS;
 
-__global__ void __launch_bounds__(kUpThreads)
-rf_upsample_q16(const double *__restrict__ h, const double *__restrict__ U, int64_t nout,
-                int64_t hop, int C, int16_t *__restrict__ out) {
-    extern __shared__ double sm[];
-    double *sh = sm;                 // [kUpTM][C+1]
-    double *su = sm + kUpTM * (C + 1);  // [kUpTN][C+1]
-    const int64_t f0 = (int64_t)blockIdx.y * kUpTM, j0 = (int64_t)blockIdx.x * kUpTN;
-    for (int idx = threadIdx.x; idx < kUpTM * C; idx += blockDim.x) {
-        int r = idx / C, k = idx % C;
-        sh[r * (C + 1) + k] = (f0 + r < nout) ? h[(f0 + r) * C + k] : 0.0;
+    // All staging is asynchronous (cp.async, 8-byte granules, zero-fill outside the
+    // valid frame range): the tile + halo and the weight slice in group 0, this CTA's
+    // upsampler slice in group 1, which is only waited for after the conv layers.
+    for (int w = threadIdx.x / C; w < W; w += kThreads / C) {
+        const int c = threadIdx.x % C;
+        const int64_t g = gbase + w;
+        const bool in = g >= A.vlo && g < A.vhi;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(act + w * C + c);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst),
+                     "l"(A.latent + (in ? g * C + c : 0)), "r"(in ? 8 : 0));
     }
-    for (int idx = threadIdx.x; idx < kUpTN * C; idx += blockDim.x) {
-        int r = idx / C, k = idx % C;
-        su[r * (C + 1) + k] = (j0 + r < hop) ? U[(j0 + r) * C + k] : 0.0;
+    for (int rest = threadIdx.x / CS; rest < L * 3 * C; rest += kThreads / CS) {
+        const int cc = threadIdx.x % CS;                // rest = (l*3 + tap)*C + k
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(wts + rest * CS + cc);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                     "l"(A.kernels + (int64_t)rest * C + c0 + cc));
     }
-    __syncthreads();
-    const int tr = threadIdx.x / 32;  // 8 row groups of 4 frames
-    const int tc = threadIdx.x % 32;  // 32 column groups of 4 samples (strided by 32)
-    double acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    for (int k = 0; k < C; ++k) {
-        double hv[4], uv[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) hv[a] = sh[(tr * 4 + a) * (C + 1) + k];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) uv[b] = su[(tc + 32 * b) * (C + 1) + k];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fma(hv[a], uv[b], acc[a][b]);
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        int64_t f = f0 + tr * 4 + a;
-        if (f >= nout) continue;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            int64_t j = j0 + tc + 32 * b;
-            if (j < hop) out[f * hop + j] = quantize_pcm(acc[a][b]);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const int j0 = rank * jper;
+    const int jn = (int)(j0 + jper < A.hop ? jper : A.hop - j0);
+    for (int c = 0; c < C; ++c) {
+        const double *src = A.upT + (int64_t)c * A.hop + j0;
+        for (int jj = threadIdx.x; jj < jn; jj += kThreads) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(ups + (size_t)c * jper + jj);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src + jj));
         }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+
+    const int grp = threadIdx.x / kKS, sub = threadIdx.x % kKS;
+    constexpr int ngrp = kThreads / kKS;
+    int lo = 0, hi = W;
+    for (int l = 0; l < L; ++l) {
+        const int d = A.dil[l];
+        const int olo = lo + d, ohi = hi - d;
+        const double *K = wts + (size_t)l * 3 * C * CS;
+        const int nout = (ohi - olo) * CS;
+        double *part = part0 + (size_t)(l & 1) * W * CS;  // double-buffered across layers
+        for (int base = 0; base < nout; base += ngrp) {
+            const int o = base + grp;
+            const bool live = o < nout;
+            const int w = live ? olo + o / CS : olo;
+            const int cc = live ? o % CS : 0;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            if (live) {
+                // lane `sub` takes input channels sub, sub+8, ... so the 8 lanes of a
+                // group read consecutive doubles of both operands (no bank conflicts)
+                const double *r0 = act + (w - d) * C + sub;
+                const double *r1 = act + w * C + sub;
+                const double *r2 = act + (w + d) * C + sub;
+                const double *kk = K + sub * CS + cc;
+#pragma unroll
+                for (int k = 0; k < KPER; ++k) {
+                    s0 = fma(r0[k * kKS], kk[(0 * C + k * kKS) * CS], s0);
+                    s1 = fma(r1[k * kKS], kk[(1 * C + k * kKS) * CS], s1);
+                    s2 = fma(r2[k * kKS], kk[(2 * C + k * kKS) * CS], s2);
+                }
+            }
+            double s = __dadd_rn(__dadd_rn(s0, s1), s2);
+            // fixed 8-lane reduction tree (the lanes of a group are adjacent)
+            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+            if (live && sub == 0) {
+                const int64_t g = gbase + w;
+                part[w * CS + cc] = (g >= A.vlo && g < A.vhi) ? tanh(s) : 0.0;
+            }
+        }
+        cluster.sync();   // every CTA's slice of layer l is complete (and, because each
+                          // CTA computed layer l after gathering layer l-1, nobody still
+                          // reads the other `part` buffer, which layer l+1 overwrites)
+        // gather all slices of rows [olo, ohi) through DSMEM, 4 remote loads in flight
+        const bool last = l == L - 1;
+        constexpr int RPI = kThreads / C;             // rows per pass
+        const int c = threadIdx.x % C;
+        const double *rp = cluster.map_shared_rank(part, c / CS);
+        for (int w0 = olo + threadIdx.x / C; w0 < ohi; w0 += 4 * RPI) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int w = w0 + u * RPI;
+                v[u] = w < ohi ? rp[w * CS + c % CS] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int w = w0 + u * RPI;
+                if (w < ohi) {
+                    if (last)
+                        hT[c * kTF + (w - olo)] = v[u];
+                    else
+                        act[w * C + c] = v[u];
+                }
+            }
+        }
+        __syncthreads();  // this CTA's act is complete before computing the next layer
+        lo = olo;
+        hi = ohi;
+    }
+    cluster.sync();   // no CTA may exit while a peer could still read its `part`
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    // pcm[f][j] = quantize(sum_c h[f][c] U[j][c]) for this CTA's samples
+    const int64_t fmax = A.nout - tile * kTF < kTF ? A.nout - tile * kTF : kTF;
+    for (int jj = threadIdx.x; jj < jn; jj += kThreads) {
+        double acc[kTF];
+#pragma unroll
+        for (int f = 0; f < kTF; ++f) acc[f] = 0.0;
+#pragma unroll 4
+        for (int c = 0; c < C; ++c) {
+            const double u = ups[c * jper + jj];
+            const double2 *hv = reinterpret_cast<const double2 *>(hT + c * kTF);
+#pragma unroll
+            for (int f2 = 0; f2 < kTF / 2; ++f2) {
+                const double2 h = hv[f2];
+                acc[2 * f2] = fma(h.x, u, acc[2 * f2]);
+                acc[2 * f2 + 1] = fma(h.y, u, acc[2 * f2 + 1]);
+            }
+        }
+        const int64_t j = j0 + jj;
+#pragma unroll
+        for (int f = 0; f < kTF; ++f)
+            if (f < fmax) A.out[(tile * kTF + f) * A.hop + j] = quantize_pcm(acc[f]);
     }
 }
 
@@ -150,21 +209,27 @@ rf_upsample_q16(const double *__restrict__ h, const double *__restrict__ U, int6
 using namespace rf;
 
 extern "C" int64_t rf_decode_workspace_bytes(int64_t out_frames, int64_t channels) {
-    return ((out_frames * channels * 8) + 255) / 256 * 256;
+    (void)out_frames;
+    (void)channels;
+    return 256;  // the fused kernel keeps every intermediate on chip
 }
 
 extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t channels,
                                 const double *kernels, const int32_t *dilations, int32_t n_layers,
-                                const double *upsample, int64_t hop, int64_t start, int64_t stop,
+                                const double *upsample_t, int64_t hop, int64_t start, int64_t stop,
                                 int64_t overlap, int32_t full, int16_t *out, void *workspace,
                                 int64_t workspace_bytes, void *stream) {
-    if (!latent || !kernels || !dilations || !upsample || !out || !workspace) {
+    (void)workspace;
+    (void)workspace_bytes;
+    if (!latent || !kernels || !dilations || !upsample_t || !out) {
         set_error("rf_decode_window: null argument");
         return RF_EINVAL;
     }
-    if (channels < 1 || channels > kMaxC || n_layers < 1 || n_layers > RF_MAX_CODEC_LAYERS || hop < 1) {
-        set_error("rf_decode_window: unsupported shape (C=%lld, L=%d, hop=%lld)", (long long)channels,
-                  n_layers, (long long)hop);
+    const bool pow2 = channels >= kNC && (channels & (channels - 1)) == 0;
+    if (channels < 1 || channels > kMaxC || !pow2 || n_layers < 1 ||
+        n_layers > RF_MAX_CODEC_LAYERS || hop < 1) {
+        set_error("rf_decode_window: unsupported shape (C=%lld must be a power of two in [%d, %d], L=%d, hop=%lld)",
+                  (long long)channels, kNC, kMaxC, n_layers, (long long)hop);
         return RF_EINVAL;
     }
     if (!(0 <= start && start < stop && stop <= frames) || overlap < 0) {
@@ -172,16 +237,11 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
                   (long long)stop, (long long)frames);
         return RF_EINVAL;
     }
-    const int64_t nout = stop - start;
-    if (workspace_bytes < rf_decode_workspace_bytes(nout, channels)) {
-        set_error("rf_decode_window: workspace too small");
-        return RF_EWORKSPACE;
-    }
-    cudaStream_t st = (cudaStream_t)stream;
-    ConvArgs A{};
+    DecodeArgs A{};
     A.latent = latent;
     A.frames = frames;
-    A.C = channels;
+    A.C = (int)channels;
+    A.CS = (int)channels / kNC;
     A.kernels = kernels;
     A.L = n_layers;
     int rfield = 0;
@@ -203,24 +263,36 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
         A.vhi = hi < frames ? hi : frames;
     }
     A.start = start;
-    A.nout = nout;
-    A.h = (double *)workspace;
-    const int W = kConvTile + 2 * rfield;
-    size_t smem = (size_t)2 * W * channels * sizeof(double);
-    if (smem > 200 * 1024) {
-        set_error("rf_decode_window: receptive field too large for one tile");
+    A.nout = stop - start;
+    A.upT = upsample_t;
+    A.hop = hop;
+    A.out = out;
+    const int W = kTF + 2 * rfield;
+    const int64_t jper = (hop + kNC - 1) / kNC;
+    size_t smem = ((size_t)W * channels + (size_t)2 * W * A.CS + (size_t)n_layers * 3 * channels * A.CS +
+                   (size_t)channels * kTF + (size_t)channels * jper) * sizeof(double);
+    if (smem > 220 * 1024) {
+        set_error("rf_decode_window: receptive field / hop too large for one tile (%zu B smem)", smem);
         return RF_EINVAL;
     }
-    RF_TRY_CUDA(cudaFuncSetAttribute(rf_conv_stack, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    unsigned nblk = (unsigned)((nout + kConvTile - 1) / kConvTile);
-    rf_conv_stack<<<nblk, kConvThreads, smem, st>>>(A);
-    RF_TRY_LAUNCH("rf_conv_stack");
-    size_t smem_up = (size_t)(kUpTM + kUpTN) * (channels + 1) * sizeof(double);
-    RF_TRY_CUDA(cudaFuncSetAttribute(rf_upsample_q16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_up));
-    dim3 g((unsigned)((hop + kUpTN - 1) / kUpTN), (unsigned)((nout + kUpTM - 1) / kUpTM));
-    rf_upsample_q16<<<g, kUpThreads, smem_up, st>>>(A.h, upsample, nout, hop, (int)channels, out);
-    RF_TRY_LAUNCH("rf_upsample_q16");
+    void (*kern)(DecodeArgs) = channels == 8    ? rf_decode_cluster<8>
+                               : channels == 16 ? rf_decode_cluster<16>
+                               : channels == 32 ? rf_decode_cluster<32>
+                                                : rf_decode_cluster<64>;
+    RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t tiles = (A.nout + kTF - 1) / kTF;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(tiles * kNC));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kNC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     return RF_OK;
 }

@@ -6,21 +6,22 @@
 //
 // numpy's ziggurat consumes a data-dependent number of 64-bit words per output
 // (1 on the fast path, 2 per wedge attempt, 1+2k for a k-iteration tail), so the
-// stream offset of output i depends on every earlier output.  The GPU resolves it
-// with a finite-state scan:
-//   pass 1 (rf_zig_classify): every stream position p is classified independently
-//     as if a draw started there -> len[p] (words consumed, following wedge
-//     restarts) and val[p].  Position p acts on the state "distance to the next draw
-//     start" s as  f_p(0) = len[p]-1, f_p(s) = s-1.  Each thread composes the maps of
-//     its 16 positions into a 16-entry nibble table (states 0..15), a block scan
-//     composes thread tables, and each block publishes its aggregate
-//     (exit state, number of draw starts) for all 16 entry states.
-//   pass 2 (rf_zig_scatter): a block folds the aggregates of the blocks before it
-//     (draw start state 0 at position 0), then walks its positions and writes
-//     out[rank] = val[p] for every draw start p with rank < n.
-// A draw that needs more than RF_ZIG_MAX_LEN words (a >= 8-iteration tail loop,
-// ~1e-12 per position) cannot be represented by the 16-state tables; pass 1 flags
-// its draw and pass 2 resolves that draw with a sequential walk instead.
+// stream offset of output i depends on every earlier output.  Two passes over the
+// stream positions of every draw in the batch resolve it:
+//   pass 1 (rf_zig_classify): one thread per Philox4x64-10 block (4 positions); every
+//     position p is classified as if a draw started there -> len[p] (words consumed,
+//     following wedge restarts) and val[p].  The slow paths read their extra words from
+//     a register window (own block + the next thread's block, by shuffle).  Per block
+//     of 512 positions the rare multi-word positions are compacted into a sorted list
+//     that 16 lanes walk, one per entry state e (positions already consumed by the
+//     previous block's last draw): the block aggregate (exit state, draw starts)[e].
+//     The last block of a draw to finish (threadfence + counter) scans the draw's
+//     aggregates from state 0 and publishes every block's entry state and output base.
+//   pass 2 (rf_zig_scatter): each block re-walks its multi list with its entry state
+//     and writes out[base + rank] = val[p] for every draw start p.
+// A draw needing more than kZigMaxLen words (a >= 8-iteration tail loop, ~1e-12 per
+// position) does not fit the 16-state tables; pass 1 flags it and pass 2 resolves that
+// draw with a sequential walk instead.
 #include <math.h>
 #include <math_constants.h>
 
@@ -29,8 +30,8 @@
 
 namespace rf {
 
-constexpr int kZigThreads = 256;
-constexpr int kZigPerThread = 16;
+constexpr int kZigThreads = 128;
+constexpr int kZigPerThread = 4;   // one Philox4x64-10 block per thread
 constexpr int kZigBlock = kZigThreads * kZigPerThread;  // stream positions per block
 constexpr int kZigMaxLen = 16;
 constexpr int kMaxDrawsPerLaunch = 24;
@@ -49,15 +50,18 @@ struct BlockAgg {
     uint16_t cnt[16];   // draw starts inside the block for entry state e
 };
 
-__device__ __forceinline__ int nib(uint64_t t, int e) { return (int)((t >> (4 * e)) & 0xF); }
+struct BlockEntry {
+    int32_t state;      // positions of this block consumed by the previous draw
+    int32_t pad;
+    int64_t base;       // output index of this block's first draw start
+};
 
-// (first a, then b)
-__device__ __forceinline__ uint64_t compose(uint64_t a, uint64_t b) {
-    uint64_t r = 0;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) r |= (uint64_t)nib(b, nib(a, e)) << (4 * e);
-    return r;
-}
+struct DrawCtl {
+    int32_t done;       // pass-1 blocks finished (last one scans)
+    int32_t long_len;   // a draw needed > kZigMaxLen words
+};
+
+__device__ __forceinline__ int nib(uint64_t t, int e) { return (int)((t >> (4 * e)) & 0xF); }
 
 __device__ __forceinline__ int find_draw(const DrawBatch &B, int64_t blk) {
     int d = 0;
@@ -165,13 +169,30 @@ __device__ __noinline__ double glibc_log1p_fma(double x) {
     return __fma_rn(kd, ln2_hi, -t);
 }
 
-// A full draw starting at stream position p (numpy random_standard_normal, every
-// branch).  Used for the 1-2% of positions that miss the fast path.
-__device__ __noinline__ void zig_slow(uint64_t k0, uint64_t k1, uint64_t p, const ZigSmem &z,
-                                      uint32_t *len_out, double *val_out) {
-    uint64_t q = p;
+// A full draw starting at window index q (numpy random_standard_normal, every branch),
+// for the ~1.2% of positions that miss the fast path.  Words come from the 8-word
+// register window `win` (valid for indices < nwin) and are recomputed past it.
+struct Window {
+    uint64_t w[8];
+    int nwin;
+    uint64_t base;  // stream position of w[0]
+};
+
+__device__ __forceinline__ uint64_t win_word(const Window &W, uint64_t k0, uint64_t k1, int i) {
+    if (i < W.nwin) {
+        uint64_t r = W.w[0];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) r = i == k ? W.w[k] : r;
+        return r;
+    }
+    return philox_word(k0, k1, W.base + (uint64_t)i);
+}
+
+__device__ __noinline__ void zig_slow(const Window &W, uint64_t k0, uint64_t k1, int q,
+                                      const ZigSmem &z, uint32_t *len_out, double *val_out) {
+    int qq = q;
     for (;;) {
-        uint64_t r = philox_word(k0, k1, q);
+        uint64_t r = win_word(W, k0, k1, qq);
         int idx = (int)(r & 0xff);
         r >>= 8;
         int sign = (int)(r & 1);
@@ -179,47 +200,151 @@ __device__ __noinline__ void zig_slow(uint64_t k0, uint64_t k1, uint64_t p, cons
         double x = __dmul_rn((double)rabs, z.wi[idx]);
         if (sign) x = -x;
         if (rabs < z.ki[idx]) {
-            *len_out = (uint32_t)(q + 1 - p);
+            *len_out = (uint32_t)(qq + 1 - q);
             *val_out = x;
             return;
         }
         if (idx == 0) {
-            uint64_t q2 = q + 1;
+            int q2 = qq + 1;
             for (;;) {
-                double u1 = u64_to_unit_double(philox_word(k0, k1, q2));
-                double u2 = u64_to_unit_double(philox_word(k0, k1, q2 + 1));
+                double u1 = u64_to_unit_double(win_word(W, k0, k1, q2));
+                double u2 = u64_to_unit_double(win_word(W, k0, k1, q2 + 1));
                 q2 += 2;
                 double xx = __dmul_rn(-RF_ZIG_NOR_INV_R, glibc_log1p_fma(-u1));
                 double yy = -glibc_log1p_fma(-u2);
                 if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
-                    *len_out = (uint32_t)(q2 - p);
+                    *len_out = (uint32_t)(q2 - q);
                     double m = __dadd_rn(RF_ZIG_NOR_R, xx);
                     *val_out = ((rabs >> 8) & 1) ? -m : m;
                     return;
                 }
             }
         } else {
-            double u = u64_to_unit_double(philox_word(k0, k1, q + 1));
+            double u = u64_to_unit_double(win_word(W, k0, k1, qq + 1));
             double lhs = __dadd_rn(__dmul_rn(__dsub_rn(z.fi[idx - 1], z.fi[idx]), u), z.fi[idx]);
             double rhs = exp(__dmul_rn(__dmul_rn(-0.5, x), x));
             if (lhs < rhs) {
-                *len_out = (uint32_t)(q + 2 - p);
+                *len_out = (uint32_t)(qq + 2 - q);
                 *val_out = x;
                 return;
             }
-            q += 2;
+            qq += 2;
         }
+    }
+}
+
+struct Multi {
+    uint16_t pos;
+    uint16_t len;
+};
+
+// Compact this block's multi-word positions (position-sorted) into smem; returns the count.
+__device__ __forceinline__ int compact_multis(const uint16_t (&lens)[kZigPerThread], Multi *list,
+                                              int *warp_tot) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int mine = 0;
+#pragma unroll
+    for (int q = 0; q < kZigPerThread; ++q) mine += lens[q] > 1;
+    int incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int base = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kZigThreads / 32; ++w) {
+        base += w < warp ? warp_tot[w] : 0;
+        total += warp_tot[w];
+    }
+    int k = base + incl - mine;
+#pragma unroll
+    for (int q = 0; q < kZigPerThread; ++q) {
+        if (lens[q] > 1) {
+            list[k].pos = (uint16_t)(t * kZigPerThread + q);
+            list[k].len = lens[q];
+            ++k;
+        }
+    }
+    __syncthreads();
+    return total;
+}
+
+// Prefix of a draw's block aggregates from entry state 0, by the draw's last pass-1
+// block: each thread composes a contiguous chunk into a 16-state (exit, count) table,
+// a Kogge-Stone scan composes the chunk tables, and each thread then walks its chunk
+// with its exact entry state, writing every block's (entry state, output base).
+__device__ void draw_prefix(const BlockAgg *__restrict__ aggs, BlockEntry *__restrict__ entries,
+                            int64_t nblk) {
+    __shared__ uint64_t tex[2][kZigThreads];
+    __shared__ uint32_t tcnt[2][kZigThreads][16];
+    const int t = threadIdx.x;
+    const int64_t ch = (nblk + kZigThreads - 1) / kZigThreads;
+    const int64_t lo = t * ch, hi = lo + ch < nblk ? lo + ch : nblk;
+    uint64_t ex = 0xFEDCBA9876543210ULL;
+    uint32_t cnt[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) cnt[e] = 0;
+    for (int64_t i = lo; i < hi; ++i) {
+        const uint64_t bex = aggs[i].exit;
+        uint64_t nex = 0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int s = nib(ex, e);
+            cnt[e] += aggs[i].cnt[s];
+            nex |= (uint64_t)nib(bex, s) << (4 * e);
+        }
+        ex = nex;
+    }
+    int buf = 0;
+    tex[buf][t] = ex;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) tcnt[buf][t][e] = cnt[e];
+    __syncthreads();
+    // inclusive scan: table[t] = table[t - off] then table[t]
+    for (int off = 1; off < kZigThreads; off <<= 1) {
+        const int nb = buf ^ 1;
+        if (t >= off) {
+            const uint64_t aex = tex[buf][t - off], bex = tex[buf][t];
+            uint64_t nex = 0;
+            for (int e = 0; e < 16; ++e) {
+                const int s = nib(aex, e);
+                tcnt[nb][t][e] = tcnt[buf][t - off][e] + tcnt[buf][t][s];
+                nex |= (uint64_t)nib(bex, s) << (4 * e);
+            }
+            tex[nb][t] = nex;
+        } else {
+            tex[nb][t] = tex[buf][t];
+            for (int e = 0; e < 16; ++e) tcnt[nb][t][e] = tcnt[buf][t][e];
+        }
+        __syncthreads();
+        buf = nb;
+    }
+    int s = 0;
+    int64_t base = 0;
+    if (t > 0) {
+        s = nib(tex[buf][t - 1], 0);
+        base = tcnt[buf][t - 1][0];
+    }
+    for (int64_t i = lo; i < hi; ++i) {
+        entries[i].state = s;
+        entries[i].base = base;
+        base += aggs[i].cnt[s];
+        s = nib(aggs[i].exit, s);
     }
 }
 
 // ----------------------------------------------------------------- pass 1 --------
 __global__ void __launch_bounds__(kZigThreads)
-rf_zig_classify(const __grid_constant__ DrawBatch B, uint16_t *__restrict__ len_ws, double *__restrict__ val_ws,
-                uint64_t *__restrict__ thread_tab, BlockAgg *__restrict__ aggs,
-                int *__restrict__ long_flag) {
+rf_zig_classify(const __grid_constant__ DrawBatch B, uint16_t *__restrict__ len_ws,
+                double *__restrict__ val_ws, BlockAgg *__restrict__ aggs,
+                BlockEntry *__restrict__ entries, DrawCtl *__restrict__ ctl) {
     __shared__ ZigSmem z;
-    __shared__ uint64_t warp_tab[kZigThreads / 32];
-    __shared__ uint64_t warp_cnt[kZigThreads / 32][4];
+    __shared__ Multi list[kZigBlock];
+    __shared__ int warp_tot[kZigThreads / 32];
+    __shared__ int am_last;
     load_zig(z);
     __syncthreads();
 
@@ -227,114 +352,82 @@ rf_zig_classify(const __grid_constant__ DrawBatch B, uint16_t *__restrict__ len_
     const int d = find_draw(B, blk);
     const int64_t j = blk - B.block_off[d];
     const uint64_t k0 = B.k0[d], k1 = B.k1[d];
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int t = threadIdx.x, lane = t & 31;
     const uint64_t p0 = (uint64_t)j * kZigBlock + (uint64_t)t * kZigPerThread;
     const int64_t ws0 = B.pos_off[d] + (int64_t)j * kZigBlock + (int64_t)t * kZigPerThread;
 
-    uint64_t tab = 0xFEDCBA9876543210ULL;  // identity
-    uint64_t cnt_lo = 0, cnt_hi = 0;       // byte e = starts seen for entry state e
-    bool any_long = false;
+    Window W;
+    const u64x4 wv = philox4x64_10((p0 >> 2) + 1, 0, 0, 0, k0, k1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        W.w[i] = wv.v[i];
+        W.w[4 + i] = __shfl_down_sync(0xffffffffu, wv.v[i], 1);
+    }
+    W.nwin = lane < 31 ? 8 : 4;
+    W.base = p0;
+
     uint16_t lens[kZigPerThread];
     double vals[kZigPerThread];
-#pragma unroll
-    for (int b = 0; b < kZigPerThread / 4; ++b) {
-        uint64_t blk_ctr = ((p0 >> 2) + b) + 1;
-        u64x4 w = philox4x64_10(blk_ctr, 0, 0, 0, k0, k1);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int q = b * 4 + i;
-            uint64_t r = w.v[i];
-            int idx = (int)(r & 0xff);
-            uint64_t rr = r >> 8;
-            uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-            double x = __dmul_rn((double)rabs, z.wi[idx]);
-            if (rr & 1) x = -x;
-            uint32_t len = 1;
-            if (!(rabs < z.ki[idx])) zig_slow(k0, k1, p0 + q, z, &len, &x);
-            if (len > kZigMaxLen) any_long = true;
-            lens[q] = (uint16_t)(len > 0xFFFF ? 0xFFFF : len);
-            vals[q] = x;
-            // state map of this position applied after `tab`
-            uint64_t tt = tab | (tab >> 1);
-            tt |= tt >> 2;
-            uint64_t zmask = ~tt & 0x1111111111111111ULL;  // nibbles equal to 0
-            uint64_t lm1 = (uint64_t)((len - 1) > 15 ? 15 : (len - 1));
-            tab = (tab - (0x1111111111111111ULL & ~zmask)) | (zmask * lm1);
-            // count starts per entry state: spread nibble flags into byte lanes
-            uint64_t lo = zmask & 0xFFFFFFFFULL, hi = zmask >> 32;
-            lo = (lo | (lo << 16)) & 0x0000FFFF0000FFFFULL;
-            lo = (lo | (lo << 8)) & 0x00FF00FF00FF00FFULL;
-            lo = (lo | (lo << 4)) & 0x0F0F0F0F0F0F0F0FULL;
-            hi = (hi | (hi << 16)) & 0x0000FFFF0000FFFFULL;
-            hi = (hi | (hi << 8)) & 0x00FF00FF00FF00FFULL;
-            hi = (hi | (hi << 4)) & 0x0F0F0F0F0F0F0F0FULL;
-            cnt_lo += lo;
-            cnt_hi += hi;
-        }
-    }
-    // write classification
+    bool any_long = false;
 #pragma unroll
     for (int q = 0; q < kZigPerThread; ++q) {
-        len_ws[ws0 + q] = lens[q];
-        val_ws[ws0 + q] = vals[q];
+        const uint64_t r = W.w[q];
+        const int idx = (int)(r & 0xff);
+        const uint64_t rr = r >> 8;
+        const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+        double x = __dmul_rn((double)rabs, z.wi[idx]);
+        if (rr & 1) x = -x;
+        uint32_t len = 1;
+        if (!(rabs < z.ki[idx])) zig_slow(W, k0, k1, q, z, &len, &x);
+        any_long |= len > kZigMaxLen;
+        lens[q] = (uint16_t)(len > 0xFFFF ? 0xFFFF : len);
+        vals[q] = x;
     }
-    if (any_long) atomicOr(long_flag + d, 1);
+    *reinterpret_cast<ushort4 *>(len_ws + ws0) = make_ushort4(lens[0], lens[1], lens[2], lens[3]);
+    *reinterpret_cast<double2 *>(val_ws + ws0) = make_double2(vals[0], vals[1]);
+    *reinterpret_cast<double2 *>(val_ws + ws0 + 2) = make_double2(vals[2], vals[3]);
+    if (any_long) atomicOr(&ctl[d].long_len, 1);
 
-    // exclusive scan of thread tables (composition) within the block
-    uint64_t incl = tab;
+    const int nm = compact_multis(lens, list, warp_tot);
+    if (t < 16) {
+        int covered_end = t, covered = t;
+        for (int i = 0; i < nm; ++i) {
+            const int p = list[i].pos;
+            if (p >= covered_end) {
+                const int end = p + list[i].len;
+                covered += (end < kZigBlock ? end : kZigBlock) - (p + 1);
+                covered_end = end;
+            }
+        }
+        const int ex = covered_end > kZigBlock ? covered_end - kZigBlock : 0;
+        uint64_t exmask = (uint64_t)(ex > 15 ? 15 : ex) << (4 * t);
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        uint64_t other = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl = compose(other, incl);
+        for (int off = 8; off > 0; off >>= 1) exmask |= __shfl_xor_sync(0x0000ffffu, exmask, off);
+        aggs[blk].cnt[t] = (uint16_t)(kZigBlock - covered);
+        if (t == 0) aggs[blk].exit = exmask;
     }
-    if (lane == 31) warp_tab[warp] = incl;
+    // last block of this draw to finish computes the draw's block prefix
+    __threadfence();
     __syncthreads();
-    uint64_t warp_prefix = 0xFEDCBA9876543210ULL;
-    for (int w = 0; w < warp; ++w) warp_prefix = compose(warp_prefix, warp_tab[w]);
-    uint64_t lane_excl = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) lane_excl = 0xFEDCBA9876543210ULL;
-    const uint64_t entry_tab = compose(warp_prefix, lane_excl);
-    thread_tab[blk * kZigThreads + t] = entry_tab;
-
-    // per-entry-state counts of the whole block: sum_t cnt_t[entry_tab(e)]
-    uint64_t c4[4] = {0, 0, 0, 0};  // 16-bit lanes, entry e in word e/4, lane e%4
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        int s = nib(entry_tab, e);
-        uint64_t c = s < 8 ? (cnt_lo >> (8 * s)) & 0xFF : (cnt_hi >> (8 * (s - 8))) & 0xFF;
-        c4[e >> 2] += c << (16 * (e & 3));
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) c4[k] += __shfl_xor_sync(0xffffffffu, c4[k], off);
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) warp_cnt[warp][k] = c4[k];
-    }
+    const int64_t nblk = B.block_off[d + 1] - B.block_off[d];
+    if (t == 0) am_last = atomicAdd(&ctl[d].done, 1) == (int)nblk - 1;
     __syncthreads();
-    if (t == 0) {
-        uint64_t tot = 0xFEDCBA9876543210ULL;
-        for (int w = 0; w < kZigThreads / 32; ++w) tot = compose(tot, warp_tab[w]);
-        BlockAgg a;
-        a.exit = tot;
-        uint64_t s4[4] = {0, 0, 0, 0};
-        for (int w = 0; w < kZigThreads / 32; ++w)
-            for (int k = 0; k < 4; ++k) s4[k] += warp_cnt[w][k];
-        for (int e = 0; e < 16; ++e) a.cnt[e] = (uint16_t)((s4[e >> 2] >> (16 * (e & 3))) & 0xFFFF);
-        aggs[blk] = a;
+    if (am_last) {
+        __threadfence();
+        draw_prefix(aggs + B.block_off[d], entries + B.block_off[d], nblk);
     }
 }
 
 // ----------------------------------------------------------------- pass 2 --------
 __global__ void __launch_bounds__(kZigThreads)
-rf_zig_scatter(const __grid_constant__ DrawBatch B, const uint16_t *__restrict__ len_ws, const double *__restrict__ val_ws,
-               const uint64_t *__restrict__ thread_tab, const BlockAgg *__restrict__ aggs,
-               const int *__restrict__ long_flag, uint32_t *__restrict__ status) {
-    __shared__ int s_entry;
-    __shared__ long long s_base;
-    __shared__ int warp_sum[kZigThreads / 32];
+rf_zig_scatter(const __grid_constant__ DrawBatch B, const uint16_t *__restrict__ len_ws,
+               const double *__restrict__ val_ws, const BlockAgg *__restrict__ aggs,
+               const BlockEntry *__restrict__ entries, const DrawCtl *__restrict__ ctl,
+               uint32_t *__restrict__ status) {
+    __shared__ int warp_tot[kZigThreads / 32];
+    __shared__ Multi list[kZigBlock];
+    __shared__ uint16_t cov_lo[kZigBlock], cov_hi[kZigBlock];
+    __shared__ int n_cov;
     const int64_t blk = blockIdx.x;
     const int d = find_draw(B, blk);
     const int64_t j = blk - B.block_off[d];
@@ -344,8 +437,8 @@ rf_zig_scatter(const __grid_constant__ DrawBatch B, const uint16_t *__restrict__
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t wsd = B.pos_off[d];
 
-    if (long_flag[d]) {
-        // Sequential resolution of the whole draw (astronomically rare).
+    if (ctl[d].long_len) {
+        // Sequential resolution of the whole draw (a >= 8-iteration tail loop somewhere).
         if (j == 0 && t == 0) {
             int64_t p = 0, i = 0, m = nblk * kZigBlock;
             while (i < n && p < m) {
@@ -357,50 +450,53 @@ rf_zig_scatter(const __grid_constant__ DrawBatch B, const uint16_t *__restrict__
         }
         return;
     }
+    const BlockEntry be = entries[blk];
+    if (j == nblk - 1 && t == 0 && be.base + aggs[blk].cnt[be.state] < n)
+        atomicOr(status, RF_STATUS_NOISE_SHORT);
+    if (be.base >= n) return;
+    const int64_t ws0 = wsd + j * kZigBlock + (int64_t)t * kZigPerThread;
+    const ushort4 l4 = *reinterpret_cast<const ushort4 *>(len_ws + ws0);
+    const uint16_t lens[kZigPerThread] = {l4.x, l4.y, l4.z, l4.w};
+    const int nm = compact_multis(lens, list, warp_tot);
     if (t == 0) {
-        int s = 0;
-        long long base = 0;
-        const BlockAgg *a = aggs + B.block_off[d];
-        for (int64_t i = 0; i < j; ++i) {
-            base += a[i].cnt[s];
-            s = nib(a[i].exit, s);
+        int covered_end = be.state, k = 0;
+        for (int i = 0; i < nm; ++i) {
+            const int p = list[i].pos;
+            if (p >= covered_end) {
+                covered_end = p + list[i].len;
+                cov_lo[k] = (uint16_t)(p + 1);
+                cov_hi[k] = (uint16_t)(covered_end < kZigBlock ? covered_end : kZigBlock);
+                ++k;
+            }
         }
-        s_entry = s;
-        s_base = base;
-        if (j == nblk - 1 && base + a[j].cnt[s] < n) atomicOr(status, RF_STATUS_NOISE_SHORT);
+        n_cov = k;
     }
     __syncthreads();
-    const int64_t base = s_base;
-    if (base >= n) return;
-    int s = nib(thread_tab[blk * kZigThreads + t], s_entry);
-    const int64_t ws0 = wsd + j * kZigBlock + (int64_t)t * kZigPerThread;
-    uint16_t lens[kZigPerThread];
-#pragma unroll
-    for (int q = 0; q < kZigPerThread; ++q) lens[q] = len_ws[ws0 + q];
+    const int ncov = n_cov;
     uint32_t starts = 0;
     int c = 0;
 #pragma unroll
     for (int q = 0; q < kZigPerThread; ++q) {
-        if (s == 0) {
+        const int p = t * kZigPerThread + q;
+        bool cov = p < be.state;
+        for (int i = 0; i < ncov && !cov; ++i) cov = p >= cov_lo[i] && p < cov_hi[i];
+        if (!cov) {
             starts |= 1u << q;
             ++c;
-            s = lens[q] - 1;
-        } else {
-            --s;
         }
     }
-    // block exclusive scan of c
     int incl = c;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         int o = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += o;
     }
-    if (lane == 31) warp_sum[warp] = incl;
+    __syncthreads();  // warp_tot reuse
+    if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
     int wp = 0;
-    for (int w = 0; w < warp; ++w) wp += warp_sum[w];
-    int64_t rank = base + wp + (incl - c);
+    for (int w2 = 0; w2 < warp; ++w2) wp += warp_tot[w2];
+    int64_t rank = be.base + wp + (incl - c);
 #pragma unroll
     for (int q = 0; q < kZigPerThread; ++q) {
         if (starts & (1u << q)) {
@@ -425,7 +521,7 @@ static int64_t draw_positions(int64_t n) {
 
 struct WsLayout {
     int64_t positions, blocks;
-    int64_t off_len, off_val, off_tab, off_agg, off_flag, total;
+    int64_t off_len, off_val, off_agg, off_ent, off_ctl, total;
 };
 
 static WsLayout layout(const rf_draw *draws, int count) {
@@ -435,10 +531,10 @@ static WsLayout layout(const rf_draw *draws, int count) {
     auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
     L.off_len = 0;
     L.off_val = al(L.off_len + L.positions * 2);
-    L.off_tab = al(L.off_val + L.positions * 8);
-    L.off_agg = al(L.off_tab + L.blocks * kZigThreads * 8);
-    L.off_flag = al(L.off_agg + L.blocks * (int64_t)sizeof(BlockAgg));
-    L.total = al(L.off_flag + kMaxDrawsPerLaunch * 4);
+    L.off_agg = al(L.off_val + L.positions * 8);
+    L.off_ent = al(L.off_agg + L.blocks * (int64_t)sizeof(BlockAgg));
+    L.off_ctl = al(L.off_ent + L.blocks * (int64_t)sizeof(BlockEntry));
+    L.total = al(L.off_ctl + kMaxDrawsPerLaunch * (int64_t)sizeof(DrawCtl));
     return L;
 }
 
@@ -447,8 +543,7 @@ static WsLayout layout(const rf_draw *draws, int count) {
 using namespace rf;
 
 extern "C" int64_t rf_normal_workspace_bytes(const rf_draw *draws, int count) {
-    // The batch is processed in chunks of kMaxDrawsPerLaunch draws reusing one
-    // workspace, so the requirement is the largest chunk.
+    // Chunks of kMaxDrawsPerLaunch draws reuse one workspace: size for the largest.
     int64_t best = 0;
     for (int c0 = 0; c0 < count; c0 += kMaxDrawsPerLaunch) {
         int c = count - c0 < kMaxDrawsPerLaunch ? count - c0 : kMaxDrawsPerLaunch;
@@ -496,14 +591,13 @@ extern "C" int rf_normal_fill(const rf_draw *draws, int count, void *workspace,
         char *ws = (char *)workspace;
         uint16_t *len_ws = (uint16_t *)(ws + L.off_len);
         double *val_ws = (double *)(ws + L.off_val);
-        uint64_t *tab = (uint64_t *)(ws + L.off_tab);
         BlockAgg *aggs = (BlockAgg *)(ws + L.off_agg);
-        int *flags = (int *)(ws + L.off_flag);
-        RF_TRY_CUDA(cudaMemsetAsync(flags, 0, kMaxDrawsPerLaunch * sizeof(int), st));
-        rf_zig_classify<<<(unsigned)blk, kZigThreads, 0, st>>>(B, len_ws, val_ws, tab, aggs, flags);
+        BlockEntry *ent = (BlockEntry *)(ws + L.off_ent);
+        DrawCtl *ctl = (DrawCtl *)(ws + L.off_ctl);
+        RF_TRY_CUDA(cudaMemsetAsync(ctl, 0, kMaxDrawsPerLaunch * sizeof(DrawCtl), st));
+        rf_zig_classify<<<(unsigned)blk, kZigThreads, 0, st>>>(B, len_ws, val_ws, aggs, ent, ctl);
         RF_TRY_LAUNCH("rf_zig_classify");
-        rf_zig_scatter<<<(unsigned)blk, kZigThreads, 0, st>>>(B, len_ws, val_ws, tab, aggs, flags,
-                                                              status);
+        rf_zig_scatter<<<(unsigned)blk, kZigThreads, 0, st>>>(B, len_ws, val_ws, aggs, ent, ctl, status);
         RF_TRY_LAUNCH("rf_zig_scatter");
     }
     return RF_OK;
