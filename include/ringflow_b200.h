@@ -120,6 +120,7 @@ typedef struct rf_row {
 #define RF_ROWF_COND_V 0x10        /* cond_x0[k] hold velocities (DiT output / seam input) */
 #define RF_ROWF_UNCOND_V 0x20      /* uncond_x0 holds the negative velocity */
 #define RF_ROWF_NO_STEP 0x40       /* velocity only (guided_velocity seam): x untouched */
+#define RF_ROWF_V_F32 0x80         /* cond/uncond velocities are float32 (DiT output) */
 
 /* rows: HOST array of `count` rows; style_offset: device [T*D] (ModelWeights). */
 int rf_tick_solve(const rf_row *rows, int count, int64_t frames, int64_t channels,
@@ -175,6 +176,79 @@ int rf_decode_window(const double *latent, int64_t frames, int64_t channels,
                      const double *upsample_t, int64_t hop, int64_t start, int64_t stop,
                      int64_t overlap, int32_t full, int16_t *out, void *workspace,
                      int64_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------ DiT GEMM (A8) ------
+ * The tensor-core GEMM of the ACE-Step-shape DiT velocity model (the reference's
+ * ToyFlowModel slot, model.py:91-152): out[M,N] = A[M,K] * B[N,K]^T with bf16 operands
+ * (both K-major, nn.Linear layout), fp32 accumulation in TMEM (tcgen05.mma fed by TMA).
+ * epilogue: 0 = store bf16, 1 = store f32, 2 = f32 gated residual
+ *   out[m,n] += gate[(m / rows_per_batch) * gate_ld + n] * acc, 3 = SwiGLU over
+ *   interleaved (gate, up) columns -> bf16 out[m, n/2], 4 = store f32 * alpha.
+ * K % 64 == 0, N % block_n == 0, block_n in {128, 256}. */
+#define RF_EPI_BF16 0
+#define RF_EPI_F32 1
+#define RF_EPI_RESID_GATE 2
+#define RF_EPI_SWIGLU 3
+#define RF_EPI_F32_SCALE 4
+int rf_gemm_bf16(const void *A, const void *B, void *out, int64_t M, int64_t N, int64_t K, int64_t lda,
+                 int64_t ldb, int64_t ldo, int32_t epilogue, const float *gate, int64_t gate_ld,
+                 int32_t rows_per_batch, float alpha, int32_t block_n, void *stream);
+
+/* Multi-head attention (flash schedule, bf16 in/out, fp32 softmax), head_dim 128:
+ * q [batch*n_q, ldq] (head h at column h*128), k/v [batch*n_k, ld] with kv head
+ * h / (heads / kv_heads); out [batch*n_q, ldo]. */
+int rf_attention_bf16(const void *q, const void *k, const void *v, void *out, int32_t batch, int32_t n_q,
+                      int32_t n_k, int32_t heads, int32_t kv_heads, int64_t ldq, int64_t ldk, int64_t ldv,
+                      int64_t ldo, void *stream);
+
+/* --------------------------------------------------- ACE-Step-shape DiT (A8) ------
+ * The velocity model that replaces the reference's ToyFlowModel for BASELINE configs
+ * 2-5 (the reference has no DiT: builder-defined ACE-Step-1.5 shape).
+ * rows = ring slots x conditions (+ unconditional rows for guidance), each with its
+ * own timestep t (its schedule's sigma[step]) and conditioning tokens. */
+typedef struct rf_dit_config {
+    int32_t latent_channels; /* 64 */
+    int32_t patch;           /* 2: tokens = frames / 2 */
+    int32_t d_model;         /* 2048 */
+    int32_t n_layers;        /* 24 */
+    int32_t n_heads;         /* 16 */
+    int32_t n_kv_heads;      /* 8 (GQA) */
+    int32_t head_dim;        /* 128 */
+    int32_t mlp_hidden;      /* 6144 (SwiGLU) */
+    int32_t n_cond_tokens;   /* 128 */
+    int32_t freq_dim;        /* 256 (sinusoidal timestep features) */
+    float rope_theta;        /* 10000 */
+    float norm_eps;          /* 1e-6 */
+} rf_dit_config;
+
+typedef struct rf_dit_weights { /* device pointers, bf16 [out, in] unless noted */
+    const void *w_in;        /* [d, patch*C] */
+    const void *w_t1;        /* [d, freq_dim] */
+    const void *w_t2;        /* [d, d] */
+    const void *w_ada;       /* [6d, d]   AdaLN-single */
+    const float *ada_table;  /* [L, 6d] f32 per-layer modulation table */
+    const void *w_qkv;       /* [L][(H + 2 Hkv) * 128, d] */
+    const void *w_o;         /* [L][d, H * 128] */
+    const void *w_qc;        /* [L][H * 128, d] */
+    const void *w_kvc;       /* [L][2 Hkv * 128, d] */
+    const void *w_oc;        /* [L][d, H * 128] */
+    const void *w_gu;        /* [L][2 F, d] rows interleaved (gate_j, up_j) */
+    const void *w_down;      /* [L][d, F] */
+    const void *w_final_ada; /* [2d, d] */
+    const void *w_out;       /* [patch*C, d] */
+    const float *ones;       /* [d] f32 ones (ungated residual) */
+} rf_dit_weights;
+
+int64_t rf_dit_workspace_bytes(const rf_dit_config *cfg, int32_t max_rows, int32_t frames);
+int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, int32_t max_rows, int32_t frames,
+                  void *workspace, int64_t workspace_bytes, void **handle, void *stream);
+int rf_dit_destroy(void *handle);
+/* x_rows/cond_rows: HOST arrays of device pointers (float64 [frames*C] latents,
+ * bf16 [n_cond_tokens, d] conditioning); t_rows: HOST float timesteps.  v_out: device
+ * f32 [rows, frames*C] or NULL for the handle's own buffer (rf_dit_output). */
+int rf_dit_forward(void *handle, int32_t rows, const double *const *x_rows, const float *t_rows,
+                   const void *const *cond_rows, float *v_out, void *stream);
+float *rf_dit_output(void *handle);
 
 /* Squared-difference reductions used by the similarity filter and tests. */
 int rf_mse(const double *a, const double *b, int64_t numel, double *out, void *stream);

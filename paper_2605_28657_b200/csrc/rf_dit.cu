@@ -1,0 +1,369 @@
+// ACE-Step-1.5-shape DiT velocity model: the batched ring-buffer forward (SURVEY.md §8(a) A8,
+// north_star (a)).  Rows are ring slots (x condition), each with its OWN timestep: the
+// per-row t enters through the timestep embedding -> AdaLN-single modulation vectors,
+// which every per-layer kernel indexes by row (m / tokens_per_row).
+//
+// Per layer (pre-norm DiT block with AdaLN-single, GQA self-attention with RoPE,
+// cross-attention to the row's conditioning tokens, SwiGLU MLP); fp32 residual stream,
+// bf16 GEMM operands with fp32 accumulation in TMEM:
+//   a   = RMSNorm(h) * (1 + scale_msa[row]) + shift_msa[row]          rf_dit_norm_mod
+//   qkv = a Wqkv^T, RoPE on q,k in the epilogue                       tcgen05 GEMM
+//   o   = Attention(q, k, v)                                          rf_attention
+//   h  += gate_msa[row] * (o Wo^T)                                    GEMM, gated-residual epi
+//   c   = RMSNorm(h);  oc = Attention(c Wqc^T, cond Wkc^T, cond Wvc^T)
+//   h  += oc Woc^T                                                    GEMM, residual epi
+//   m   = RMSNorm(h) * (1 + scale_mlp[row]) + shift_mlp[row]
+//   h  += gate_mlp[row] * (SwiGLU(m Wgu^T) Wdown^T)                   GEMM SwiGLU epi, GEMM
+// then  v = (RMSNorm(h) * (1 + scale_f[row]) + shift_f[row]) Wout^T (fp32), unpatchified.
+#include <math.h>
+
+#include <vector>
+
+#include "rf_common.cuh"
+#include "rf_gemm_host.h"
+
+#include <cuda_bf16.h>
+
+extern "C" int rf_attention_bf16(const void *q, const void *k, const void *v, void *out, int32_t batch,
+                                 int32_t n_q, int32_t n_k, int32_t heads, int32_t kv_heads, int64_t ldq,
+                                 int64_t ldk, int64_t ldv, int64_t ldo, void *stream);
+
+namespace rf {
+
+constexpr int kMaxDitRows = 64;
+
+// ------------------------------------------------------------------ kernels ------
+// RMSNorm over d (fp32 residual row) with optional AdaLN modulation, bf16 out.
+// One warp per token row; shift/scale are indexed by the row's batch entry.
+template <int D>
+__global__ void __launch_bounds__(256)
+rf_dit_norm_mod(const float *__restrict__ h, int64_t rows, int tokens, const float *__restrict__ shift,
+                const float *__restrict__ scale, int64_t mod_ld, __nv_bfloat16 *__restrict__ out, float eps) {
+    constexpr int PER = D / 32 / 4;  // float4 per lane
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float4 *x = (const float4 *)(h + row * D);
+    float4 v[PER];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        v[i] = x[lane + 32 * i];
+        ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float rstd = rsqrtf(ss / D + eps);
+    const int64_t b = row / tokens;
+    const float4 *sh = shift ? (const float4 *)(shift + b * mod_ld) : nullptr;
+    const float4 *sc = scale ? (const float4 *)(scale + b * mod_ld) : nullptr;
+    uint2 *o = (uint2 *)(out + row * D);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        float4 y = make_float4(v[i].x * rstd, v[i].y * rstd, v[i].z * rstd, v[i].w * rstd);
+        if (sc) {
+            const float4 s = sc[lane + 32 * i];
+            y.x *= 1.f + s.x;
+            y.y *= 1.f + s.y;
+            y.z *= 1.f + s.z;
+            y.w *= 1.f + s.w;
+        }
+        if (sh) {
+            const float4 s = sh[lane + 32 * i];
+            y.x += s.x;
+            y.y += s.y;
+            y.z += s.z;
+            y.w += s.w;
+        }
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(y.x, y.y), p1 = __floats2bfloat162_rn(y.z, y.w);
+        o[lane + 32 * i] = make_uint2(*(uint32_t *)&p0, *(uint32_t *)&p1);
+    }
+}
+
+struct RowPtrs {
+    const double *x[kMaxDitRows];
+    float t[kMaxDitRows];
+};
+
+// x (float64 ring rows, [T*C] each) -> bf16 patch tokens [B, N, p*C] (a flat per-row cast).
+__global__ void rf_dit_patchify(const __grid_constant__ RowPtrs R, int64_t per_row, __nv_bfloat16 *out) {
+    const int b = blockIdx.y;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i < per_row;
+         i += (int64_t)gridDim.x * blockDim.x * 2) {
+        const double2 v = *(const double2 *)(R.x[b] + i);
+        *(__nv_bfloat162 *)(out + b * per_row + i) = __floats2bfloat162_rn((float)v.x, (float)v.y);
+    }
+}
+
+// sinusoidal timestep features [cos | sin] of 1000 * t (bf16 [Bpad, F]).
+__global__ void rf_dit_tfeat(const __grid_constant__ RowPtrs R, int B, int F, __nv_bfloat16 *out) {
+    const int b = blockIdx.x, half = F / 2;
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        const float freq = expf(-logf(10000.f) * (float)i / (float)half);
+        const float arg = 1000.f * R.t[b] * freq;
+        float s, c;
+        sincosf(arg, &s, &c);
+        out[(int64_t)b * F + i] = __float2bfloat16(c);
+        out[(int64_t)b * F + half + i] = __float2bfloat16(s);
+    }
+}
+
+// out_bf16 = bf16(silu(in_f32))
+__global__ void rf_dit_silu_bf16(const float *in, __nv_bfloat16 *out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = in[i];
+        out[i] = __float2bfloat16(x / (1.f + __expf(-x)));
+    }
+}
+
+// mods[l][b][j] = table[l][j] + mod[b][j]   (j < 6d)
+__global__ void rf_dit_layer_mods(const float *table, const float *mod, float *mods, int L, int B, int W) {
+    const int64_t n = (int64_t)L * B * W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(i % W);
+        const int64_t lb = i / W;
+        const int b = (int)(lb % B), l = (int)(lb / B);
+        mods[i] = table[(int64_t)l * W + j] + mod[(int64_t)b * W + j];
+    }
+}
+
+// ----------------------------------------------------------------- runtime -------
+struct Dit {
+    rf_dit_config c;
+    rf_dit_weights w;
+    int max_rows, frames, tokens;
+    int64_t in_dim, qkv_dim, q_dim, kv_dim;
+    // workspace carve-up
+    __nv_bfloat16 *xin, *a, *qkv, *att, *qc, *cond, *kvc, *mlp, *tfeat, *tbuf;
+    float *h, *tmp, *mod, *mods, *fmod, *vout;
+    float2 *rope;
+    // GEMM plans (tensor maps at max rows)
+    GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out;
+    std::vector<GemmPlan> p_qkv, p_o, p_qc, p_kvc, p_oc, p_gu, p_down;
+};
+
+static size_t carve(char *&cur, size_t bytes) {
+    size_t off = (size_t)cur;
+    cur += (bytes + 255) / 256 * 256;
+    return off;
+}
+
+static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *d, char *base) {
+    const int64_t N = frames / c.patch, BN = (int64_t)max_rows * N, D = c.d_model;
+    const int64_t in_dim = (int64_t)c.patch * c.latent_channels;
+    const int64_t q_dim = (int64_t)c.n_heads * c.head_dim, kv_dim = (int64_t)c.n_kv_heads * c.head_dim;
+    const int64_t qkv_dim = q_dim + 2 * kv_dim;
+    const int64_t Bp = 128;  // small GEMMs (M = rows) read a padded 128-row tile
+    const int64_t rows_pad = max_rows > Bp ? max_rows : Bp;
+    char *cur = base;
+    auto take = [&](size_t bytes) { return (void *)carve(cur, bytes); };
+    void *xin = take(BN * in_dim * 2), *a = take(BN * D * 2), *qkv = take(BN * qkv_dim * 2);
+    void *att = take(BN * q_dim * 2), *qc = take(BN * q_dim * 2);
+    void *cond = take((int64_t)max_rows * c.n_cond_tokens * D * 2);
+    void *kvc = take((int64_t)max_rows * c.n_cond_tokens * 2 * kv_dim * 2);
+    void *mlp = take(BN * c.mlp_hidden * 2);
+    void *tfeat = take(rows_pad * c.freq_dim * 2), *tbuf = take(rows_pad * D * 2);
+    void *h = take(BN * D * 4), *tmp = take(rows_pad * D * 4), *mod = take(rows_pad * 6 * D * 4);
+    void *mods = take((int64_t)c.n_layers * max_rows * 6 * D * 4), *fmod = take(rows_pad * 2 * D * 4);
+    void *vout = take(BN * in_dim * 4), *rope = take(N * 64 * 8);
+    if (d) {
+        d->xin = (__nv_bfloat16 *)xin;
+        d->a = (__nv_bfloat16 *)a;
+        d->qkv = (__nv_bfloat16 *)qkv;
+        d->att = (__nv_bfloat16 *)att;
+        d->qc = (__nv_bfloat16 *)qc;
+        d->cond = (__nv_bfloat16 *)cond;
+        d->kvc = (__nv_bfloat16 *)kvc;
+        d->mlp = (__nv_bfloat16 *)mlp;
+        d->tfeat = (__nv_bfloat16 *)tfeat;
+        d->tbuf = (__nv_bfloat16 *)tbuf;
+        d->h = (float *)h;
+        d->tmp = (float *)tmp;
+        d->mod = (float *)mod;
+        d->mods = (float *)mods;
+        d->fmod = (float *)fmod;
+        d->vout = (float *)vout;
+        d->rope = (float2 *)rope;
+    }
+    return (int64_t)(cur - base);
+}
+
+__global__ void rf_dit_rope_table(float2 *rope, int N, float theta) {
+    const int n = blockIdx.x, i = threadIdx.x;  // 64 pairs of a 128-dim head
+    if (i < 64) {
+        const double inv = pow((double)theta, -2.0 * i / 128.0);
+        double s, c;
+        sincos((double)n * inv, &s, &c);
+        rope[(int64_t)n * 64 + i] = make_float2((float)c, (float)s);
+    }
+}
+
+}  // namespace rf
+
+using namespace rf;
+
+extern "C" int64_t rf_dit_workspace_bytes(const rf_dit_config *cfg, int32_t max_rows, int32_t frames) {
+    if (!cfg || max_rows < 1 || frames < 1) return -1;
+    return ws_layout(*cfg, max_rows, frames, nullptr, (char *)0) + 4096;
+}
+
+extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, int32_t max_rows, int32_t frames,
+                             void *workspace, int64_t workspace_bytes, void **handle, void *stream) {
+    if (!cfg || !w || !workspace || !handle || max_rows < 1 || max_rows > kMaxDitRows) {
+        set_error("rf_dit_create: bad arguments");
+        return RF_EINVAL;
+    }
+    const rf_dit_config &c = *cfg;
+    if (c.head_dim != 128 || c.d_model % 256 || c.mlp_hidden % 128 || frames % c.patch ||
+        (c.patch * c.latent_channels) % 128 || c.n_heads % c.n_kv_heads || c.d_model != 2048 && c.d_model != 1024 &&
+        c.d_model != 512 && c.d_model != 256) {
+        set_error("rf_dit_create: unsupported config (head_dim must be 128, d_model in {256,512,1024,2048})");
+        return RF_EINVAL;
+    }
+    if (workspace_bytes < rf_dit_workspace_bytes(cfg, max_rows, frames)) {
+        set_error("rf_dit_create: workspace too small");
+        return RF_EWORKSPACE;
+    }
+    Dit *d = new Dit();
+    d->c = c;
+    d->w = *w;
+    d->max_rows = max_rows;
+    d->frames = frames;
+    d->tokens = frames / c.patch;
+    d->in_dim = (int64_t)c.patch * c.latent_channels;
+    d->q_dim = (int64_t)c.n_heads * c.head_dim;
+    d->kv_dim = (int64_t)c.n_kv_heads * c.head_dim;
+    d->qkv_dim = d->q_dim + 2 * d->kv_dim;
+    char *base = (char *)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+    ws_layout(c, max_rows, frames, d, base);
+    const int64_t BN = (int64_t)max_rows * d->tokens, D = c.d_model, L = c.n_layers, Bmax = max_rows;
+    const int64_t Bc = (int64_t)max_rows * c.n_cond_tokens;
+    auto bn_for = [](int64_t n) { return n % 256 == 0 ? 256 : 128; };
+    int rc = 0;
+    auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
+        if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N));
+    };
+    plan(&d->p_in, d->xin, w->w_in, BN, D, d->in_dim);
+    plan(&d->p_t1, d->tfeat, w->w_t1, Bmax, D, c.freq_dim);
+    plan(&d->p_t2, d->tbuf, w->w_t2, Bmax, D, D);
+    plan(&d->p_ada, d->tbuf, w->w_ada, Bmax, 6 * D, D);
+    plan(&d->p_fada, d->tbuf, w->w_final_ada, Bmax, 2 * D, D);
+    plan(&d->p_out, d->a, w->w_out, BN, d->in_dim, D);
+    d->p_qkv.resize(L);
+    d->p_o.resize(L);
+    d->p_qc.resize(L);
+    d->p_kvc.resize(L);
+    d->p_oc.resize(L);
+    d->p_gu.resize(L);
+    d->p_down.resize(L);
+    const __nv_bfloat16 *wq = (const __nv_bfloat16 *)w->w_qkv, *wo = (const __nv_bfloat16 *)w->w_o;
+    const __nv_bfloat16 *wqc = (const __nv_bfloat16 *)w->w_qc, *wkvc = (const __nv_bfloat16 *)w->w_kvc;
+    const __nv_bfloat16 *woc = (const __nv_bfloat16 *)w->w_oc, *wgu = (const __nv_bfloat16 *)w->w_gu;
+    const __nv_bfloat16 *wdn = (const __nv_bfloat16 *)w->w_down;
+    for (int64_t l = 0; l < L; ++l) {
+        plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
+        plan(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
+        plan(&d->p_qc[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D);
+        plan(&d->p_kvc[l], d->cond, wkvc + l * 2 * d->kv_dim * D, Bc, 2 * d->kv_dim, D);
+        plan(&d->p_oc[l], d->att, woc + l * D * d->q_dim, BN, D, d->q_dim);
+        plan(&d->p_gu[l], d->a, wgu + l * 2 * (int64_t)c.mlp_hidden * D, BN, 2 * (int64_t)c.mlp_hidden, D);
+        plan(&d->p_down[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, BN, D, c.mlp_hidden);
+    }
+    if (rc) {
+        delete d;
+        return rc;
+    }
+    rf_dit_rope_table<<<d->tokens, 64, 0, (cudaStream_t)stream>>>(d->rope, d->tokens, c.rope_theta);
+    RF_TRY_LAUNCH("rf_dit_rope_table");
+    *handle = d;
+    return RF_OK;
+}
+
+extern "C" int rf_dit_destroy(void *handle) {
+    delete (Dit *)handle;
+    return RF_OK;
+}
+
+static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shift, const float *scale,
+                    int64_t mod_ld, __nv_bfloat16 *out, cudaStream_t st) {
+    const unsigned blocks = (unsigned)((rows + 7) / 8);
+    switch (d.c.d_model) {
+        case 2048: rf_dit_norm_mod<2048><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
+        case 1024: rf_dit_norm_mod<1024><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
+        case 512: rf_dit_norm_mod<512><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
+        default: rf_dit_norm_mod<256><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
+    }
+    RF_TRY_LAUNCH("rf_dit_norm_mod");
+    return RF_OK;
+}
+
+#define RF_TRY(x)              \
+    do {                       \
+        int _r = (x);          \
+        if (_r) return _r;     \
+    } while (0)
+
+extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x_rows, const float *t_rows,
+                              const void *const *cond_rows, float *v_out, void *stream) {
+    Dit *dp = (Dit *)handle;
+    if (!dp || rows < 1 || rows > dp->max_rows || !x_rows || !t_rows || !cond_rows) {
+        set_error("rf_dit_forward: bad arguments (rows=%d)", rows);
+        return RF_EINVAL;
+    }
+    const Dit &d = *dp;
+    const rf_dit_config &c = d.c;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = d.tokens, M = (int64_t)rows * N, D = c.d_model, L = c.n_layers, B = rows;
+    const int64_t W6 = 6 * D, Nc = c.n_cond_tokens;
+    RowPtrs R{};
+    for (int b = 0; b < rows; ++b) {
+        R.x[b] = x_rows[b];
+        R.t[b] = t_rows[b];
+    }
+    // patch tokens and timestep conditioning
+    rf_dit_patchify<<<dim3(64, rows), 256, 0, st>>>(R, (int64_t)d.frames * c.latent_channels, d.xin);
+    RF_TRY_LAUNCH("rf_dit_patchify");
+    rf_dit_tfeat<<<rows, 128, 0, st>>>(R, rows, c.freq_dim, d.tfeat);
+    RF_TRY_LAUNCH("rf_dit_tfeat");
+    RF_TRY(gemm_run(d.p_t1, RF_EPI_F32, d.tmp, D, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
+    rf_dit_silu_bf16<<<64, 256, 0, st>>>(d.tmp, d.tbuf, B * D);
+    RF_TRY(gemm_run(d.p_t2, RF_EPI_F32, d.tmp, D, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
+    rf_dit_silu_bf16<<<64, 256, 0, st>>>(d.tmp, d.tbuf, B * D);   // silu(temb)
+    RF_TRY(gemm_run(d.p_ada, RF_EPI_F32, d.mod, W6, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
+    RF_TRY(gemm_run(d.p_fada, RF_EPI_F32, d.fmod, 2 * D, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
+    rf_dit_layer_mods<<<256, 256, 0, st>>>(d.w.ada_table, d.mod, d.mods, (int)L, (int)B, (int)W6);
+    RF_TRY_LAUNCH("rf_dit_layer_mods");
+    // conditioning tokens of every row
+    for (int b = 0; b < rows; ++b)
+        RF_TRY_CUDA(cudaMemcpyAsync(d.cond + (int64_t)b * Nc * D, cond_rows[b], Nc * D * 2,
+                                    cudaMemcpyDeviceToDevice, st));
+    // h = in_proj(patches)
+    RF_TRY(gemm_run(d.p_in, RF_EPI_F32, d.h, D, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+    for (int64_t l = 0; l < L; ++l) {
+        const float *md = d.mods + l * B * W6;  // [B][6][D]: shift,scale,gate (msa), shift,scale,gate (mlp)
+        // self-attention
+        RF_TRY(norm_mod(d, d.h, M, md + 0 * D, md + 1 * D, W6, d.a, st));
+        RF_TRY(gemm_run(d.p_qkv[l], 5 /* bf16 + RoPE */, d.qkv, d.qkv_dim, nullptr, 0, (int)N, 1.f, st, d.rope,
+                        (int)(d.q_dim + d.kv_dim), M));
+        RF_TRY(rf_attention_bf16(d.qkv, d.qkv + d.q_dim, d.qkv + d.q_dim + d.kv_dim, d.att, (int)B, (int)N,
+                                 (int)N, c.n_heads, c.n_kv_heads, d.qkv_dim, d.qkv_dim, d.qkv_dim, d.q_dim, st));
+        RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
+        // cross-attention to the row's conditioning tokens (residual, no gate)
+        RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
+        RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+        RF_TRY(gemm_run(d.p_kvc[l], RF_EPI_BF16, d.kvc, 2 * d.kv_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, B * Nc));
+        RF_TRY(rf_attention_bf16(d.qc, d.kvc, d.kvc + d.kv_dim, d.att, (int)B, (int)N, (int)Nc, c.n_heads,
+                                 c.n_kv_heads, d.q_dim, 2 * d.kv_dim, 2 * d.kv_dim, d.q_dim, st));
+        RF_TRY(gemm_run(d.p_oc[l], RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));
+        // SwiGLU MLP
+        RF_TRY(norm_mod(d, d.h, M, md + 3 * D, md + 4 * D, W6, d.a, st));
+        RF_TRY(gemm_run(d.p_gu[l], RF_EPI_SWIGLU, d.mlp, c.mlp_hidden, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+        RF_TRY(gemm_run(d.p_down[l], RF_EPI_RESID_GATE, d.h, D, md + 5 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
+    }
+    // final AdaLN + output projection (fp32), tokens [B, N, p*C] == latent [B, T, C]
+    RF_TRY(norm_mod(d, d.h, M, d.fmod, d.fmod + D, 2 * D, d.a, st));
+    RF_TRY(gemm_run(d.p_out, RF_EPI_F32, v_out ? v_out : d.vout, d.in_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+    return RF_OK;
+}
+
+extern "C" float *rf_dit_output(void *handle) { return handle ? ((Dit *)handle)->vout : nullptr; }

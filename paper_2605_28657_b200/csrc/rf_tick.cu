@@ -57,14 +57,19 @@ __device__ __forceinline__ ElemVel velocity_elem(const rf_row &R, const double *
                                                  double x, int64_t f, int64_t i) {
     const double t = R.t_curr;
     const bool cond_v = (R.flags & RF_ROWF_COND_V) != 0;
+    const bool f32 = (R.flags & RF_ROWF_V_F32) != 0;
+    // a given velocity (DiT output: float32, or a float64 seam input)
+    auto given = [&](const double *p) -> double {
+        return f32 ? (double)reinterpret_cast<const float *>(p)[i] : p[i];
+    };
     double v;
     if (R.n_cond == 1) {
-        v = cond_v ? R.cond_x0[0][i]
+        v = cond_v ? given(R.cond_x0[0])
                    : toy_velocity(x, R.cond_x0[0][i], style[i], t, R.noise_model, R.jitter_t, i);
     } else {
         double acc = 0.0, tot = 0.0;
         for (int k = 0; k < R.n_cond; ++k) {
-            double vk = cond_v ? R.cond_x0[k][i]
+            double vk = cond_v ? given(R.cond_x0[k])
                                : toy_velocity(x, R.cond_x0[k][i], style[i], t, R.noise_model,
                                               R.jitter_t, i);
             double w = curve_or(R.cond_w[k], f, 1.0);
@@ -80,7 +85,7 @@ __device__ __forceinline__ ElemVel velocity_elem(const rf_row &R, const double *
     double neg;
     if (R.neg_kind == RF_NEG_UNCOND) {
         double vu = (R.flags & RF_ROWF_UNCOND_V)
-                        ? R.uncond_x0[i]
+                        ? given(R.uncond_x0)
                         : toy_velocity(x, R.uncond_x0[i], style[i], t, R.noise_model, R.jitter_t, i);
         if (R.flags & RF_ROWF_WRITE_RESIDUAL) {
             double res = dsub(v, vu);

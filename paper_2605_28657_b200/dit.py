@@ -1,0 +1,332 @@
+"""ACE-Step-1.5-shape DiT velocity model (BASELINE configs 2-5) on sm_100a kernels.
+
+The reference package has no DiT (its ``ToyFlowModel`` is a closed-form stand-in,
+reference model.py:91-152).  The paper's production model is ACE-Step 1.5
+(24-layer DiT, AdaLN, RMSNorm, GQA attention + MLP, 64-channel latent at 25 Hz;
+PAPER.md:44,226,242).  This module defines a builder-chosen model of that shape
+(``DiTConfig`` defaults; DESIGN.md lists every choice) with seeded random weights:
+
+    patch 2 (T=1500 frames -> 750 tokens), d=2048, 24 layers, 16 query / 8 KV heads of
+    128, SwiGLU 6144, RMSNorm, AdaLN-single timestep modulation, RoPE, cross-attention
+    to 128 conditioning tokens per prompt, fp32 residual stream.
+
+The forward is one C-ABI call (``rf_dit_forward``, csrc/rf_dit.cu): tcgen05 GEMMs fed by
+TMA with fused epilogues (RoPE, SwiGLU, AdaLN-gated residual), flash attention, fused
+RMSNorm+modulation.  ``reference_forward`` is the same network in plain PyTorch fp32 --
+the oracle the DiT is tested against (DiT parity is unpinned by the reference itself).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _device, _native
+
+
+class RfDitConfig(ctypes.Structure):
+    _fields_ = [("latent_channels", ctypes.c_int32), ("patch", ctypes.c_int32), ("d_model", ctypes.c_int32),
+                ("n_layers", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("mlp_hidden", ctypes.c_int32), ("n_cond_tokens", ctypes.c_int32),
+                ("freq_dim", ctypes.c_int32), ("rope_theta", ctypes.c_float), ("norm_eps", ctypes.c_float)]
+
+
+_WNAMES = ("w_in", "w_t1", "w_t2", "w_ada", "ada_table", "w_qkv", "w_o", "w_qc", "w_kvc", "w_oc", "w_gu", "w_down",
+           "w_final_ada", "w_out", "ones")
+
+
+class RfDitWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in _WNAMES]
+
+
+def _declare(lib):
+    if getattr(lib, "_dit_declared", False):
+        return
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.rf_dit_workspace_bytes.restype = i64
+    lib.rf_dit_workspace_bytes.argtypes = [ctypes.POINTER(RfDitConfig), i32, i32]
+    lib.rf_dit_create.restype = ctypes.c_int
+    lib.rf_dit_create.argtypes = [ctypes.POINTER(RfDitConfig), ctypes.POINTER(RfDitWeights), i32, i32, vp, i64,
+                                  ctypes.POINTER(vp), vp]
+    lib.rf_dit_destroy.restype = ctypes.c_int
+    lib.rf_dit_destroy.argtypes = [vp]
+    lib.rf_dit_forward.restype = ctypes.c_int
+    lib.rf_dit_forward.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_float), ctypes.POINTER(vp),
+                                   vp, vp]
+    lib.rf_dit_output.restype = vp
+    lib.rf_dit_output.argtypes = [vp]
+    lib.rf_attention_bf16.restype = ctypes.c_int
+    lib.rf_attention_bf16.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i64, i64, i64, i64, vp]
+    lib._dit_declared = True
+
+
+@dataclass(frozen=True)
+class DiTConfig:
+    latent_channels: int = 64
+    patch: int = 2
+    d_model: int = 2048
+    n_layers: int = 24
+    n_heads: int = 16
+    n_kv_heads: int = 8
+    head_dim: int = 128
+    mlp_hidden: int = 6144
+    n_cond_tokens: int = 128
+    freq_dim: int = 256
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-6
+    seed: int = 1234
+
+    @property
+    def in_dim(self):
+        return self.patch * self.latent_channels
+
+    def params(self) -> int:
+        d, L = self.d_model, self.n_layers
+        q, kv = self.n_heads * self.head_dim, self.n_kv_heads * self.head_dim
+        per_layer = d * (q + 2 * kv) + q * d + d * q + d * 2 * kv + q * d + 3 * d * self.mlp_hidden
+        return L * per_layer + d * self.in_dim * 2 + d * self.freq_dim + d * d + 8 * d * d
+
+    def flops_per_forward(self, rows: int, frames: int) -> float:
+        """Algorithmic FLOPs of one batched forward (GEMMs + attention matmuls)."""
+        N = frames // self.patch
+        d, L, F = self.d_model, self.n_layers, self.mlp_hidden
+        q, kv, Nc = self.n_heads * self.head_dim, self.n_kv_heads * self.head_dim, self.n_cond_tokens
+        tok = 2 * (d * (q + 2 * kv) + q * d + d * q + q * d + d * 2 * F + F * d)
+        per_row = L * (N * tok + 2 * Nc * d * 2 * kv + 4 * N * N * q + 4 * N * Nc * q)
+        per_row += 2 * N * self.in_dim * d * 2
+        return float(rows) * per_row
+
+    def small(self, **kw) -> "DiTConfig":
+        base = dict(self.__dict__)
+        base.update(dict(d_model=256, n_layers=2, n_heads=2, n_kv_heads=1, mlp_hidden=512, n_cond_tokens=32))
+        base.update(kw)
+        return DiTConfig(**base)
+
+    def to_c(self) -> RfDitConfig:
+        return RfDitConfig(self.latent_channels, self.patch, self.d_model, self.n_layers, self.n_heads,
+                           self.n_kv_heads, self.head_dim, self.mlp_hidden, self.n_cond_tokens, self.freq_dim,
+                           self.rope_theta, self.norm_eps)
+
+
+class DiTWeights:
+    """Seeded random-init weights (bf16 [out, in] matrices, fp32 tables) resident in HBM."""
+
+    def __init__(self, cfg: DiTConfig, device=None):
+        dev = device or _device.device()
+        g = torch.Generator(device=dev).manual_seed(cfg.seed)
+        d, L, F = cfg.d_model, cfg.n_layers, cfg.mlp_hidden
+        q, kv = cfg.n_heads * cfg.head_dim, cfg.n_kv_heads * cfg.head_dim
+
+        def lin(*shape, std=None):
+            fan_in = shape[-1]
+            s = std if std is not None else 1.0 / math.sqrt(fan_in)
+            return (torch.randn(*shape, generator=g, device=dev) * s).to(torch.bfloat16).contiguous()
+
+        self.w_in = lin(d, cfg.in_dim)
+        self.w_t1 = lin(d, cfg.freq_dim)
+        self.w_t2 = lin(d, d)
+        self.w_ada = lin(6 * d, d, std=0.02)
+        self.ada_table = (torch.randn(L, 6 * d, generator=g, device=dev) * 0.1).contiguous()
+        self.w_qkv = lin(L, q + 2 * kv, d)
+        self.w_o = lin(L, d, q)
+        self.w_qc = lin(L, q, d)
+        self.w_kvc = lin(L, 2 * kv, d)
+        self.w_oc = lin(L, d, q)
+        gate, up = lin(L, F, d), lin(L, F, d)
+        self.w_gu = torch.stack([gate, up], dim=2).reshape(L, 2 * F, d).contiguous()  # rows (g_j, u_j)
+        self.w_down = lin(L, d, F)
+        self.w_final_ada = lin(2 * d, d, std=0.02)
+        self.w_out = lin(cfg.in_dim, d)
+        self.ones = torch.ones(d, device=dev, dtype=torch.float32)
+
+    def to_c(self) -> RfDitWeights:
+        return RfDitWeights(*[getattr(self, n).data_ptr() for n in _WNAMES])
+
+
+class DiT:
+    """Batched DiT forward over ring rows, each with its own timestep and conditioning."""
+
+    def __init__(self, cfg: DiTConfig = DiTConfig(), frames: int = 1500, max_rows: int = 8, weights=None):
+        self.cfg = cfg
+        self.frames = frames
+        self.max_rows = max_rows
+        self.dev = _device.device()
+        self.lib = _native.load()
+        _declare(self.lib)
+        self.weights = weights or DiTWeights(cfg, self.dev)
+        self._ccfg = cfg.to_c()
+        self._cw = self.weights.to_c()
+        nbytes = self.lib.rf_dit_workspace_bytes(ctypes.byref(self._ccfg), max_rows, frames)
+        if nbytes < 0:
+            raise _native.NativeError("rf_dit_workspace_bytes failed")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        h = ctypes.c_void_p()
+        _native.check(self.lib.rf_dit_create(ctypes.byref(self._ccfg), ctypes.byref(self._cw), max_rows, frames,
+                                             self.workspace.data_ptr(), nbytes, ctypes.byref(h),
+                                             _device.current_stream_handle()), "rf_dit_create")
+        self.handle = h
+        self._cond: dict = {}
+        self.out = torch.empty(max_rows, frames, cfg.latent_channels, dtype=torch.float32, device=self.dev)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.lib.rf_dit_destroy(self.handle)
+        except Exception:
+            pass
+
+    def cond_tokens(self, prompt_hash: int) -> torch.Tensor:
+        """Conditioning tokens of a prompt: a seeded stand-in for the text/lyric encoder output."""
+        t = self._cond.get(prompt_hash)
+        if t is None:
+            g = torch.Generator(device=self.dev).manual_seed(int(prompt_hash) & ((1 << 62) - 1))
+            t = torch.randn(self.cfg.n_cond_tokens, self.cfg.d_model, generator=g, device=self.dev)
+            t = t.to(torch.bfloat16).contiguous()
+            self._cond[prompt_hash] = t
+        return t
+
+    def forward(self, xs, ts, conds, out: torch.Tensor = None) -> torch.Tensor:
+        """xs: float64 [frames, C] device latents; ts: timesteps; conds: bf16 token tensors."""
+        n = len(xs)
+        if n > self.max_rows:
+            raise ValueError(f"{n} rows > max_rows {self.max_rows}")
+        out = self.out if out is None else out
+        xp = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
+        tp = (ctypes.c_float * n)(*[float(t) for t in ts])
+        cp = (ctypes.c_void_p * n)(*[c.data_ptr() for c in conds])
+        _native.check(self.lib.rf_dit_forward(self.handle, n, xp, tp, cp, out.data_ptr(),
+                                              _device.current_stream_handle()), "rf_dit_forward")
+        return out[:n]
+
+
+# ---------------------------------------------------------------- fp32 oracle ----
+def _rmsnorm(x, eps):
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps)
+
+
+def _rope(x, cos, sin):
+    # interleaved pairs (2i, 2i+1) of each 128-dim head; x [B, N, H, 128]
+    x0, x1 = x[..., 0::2], x[..., 1::2]
+    y0 = x0 * cos - x1 * sin
+    y1 = x0 * sin + x1 * cos
+    return torch.stack([y0, y1], -1).flatten(-2)
+
+
+def reference_forward(dit: DiT, xs, ts, conds, layers: int = None) -> torch.Tensor:
+    """The same network in plain PyTorch fp32 (bf16 weights upcast), no TF32."""
+    cfg, W = dit.cfg, dit.weights
+    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        f = lambda w: w.float()  # noqa: E731
+        B, T, C = len(xs), dit.frames, cfg.latent_channels
+        N, d = T // cfg.patch, cfg.d_model
+        H, Hk, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        x = torch.stack([xx.float() for xx in xs]).reshape(B, N, cfg.in_dim)
+        x = x.bfloat16().float()
+        half = cfg.freq_dim // 2
+        freqs = torch.exp(-math.log(10000.0) * torch.arange(half, device=x.device, dtype=torch.float32) / half)
+        args = 1000.0 * torch.tensor([float(t) for t in ts], device=x.device)[:, None] * freqs[None]
+        tf = torch.cat([torch.cos(args), torch.sin(args)], -1).bfloat16().float()
+        silu = torch.nn.functional.silu
+        temb = silu(tf @ f(W.w_t1).T).bfloat16().float() @ f(W.w_t2).T
+        st = silu(temb).bfloat16().float()
+        mod = st @ f(W.w_ada).T                       # [B, 6d]
+        fmod = st @ f(W.w_final_ada).T                # [B, 2d]
+        h = x @ f(W.w_in).T                           # [B, N, d]
+        pos = torch.arange(N, device=x.device, dtype=torch.float64)
+        inv = torch.pow(torch.tensor(cfg.rope_theta, dtype=torch.float64),
+                        -2.0 * torch.arange(64, device=x.device, dtype=torch.float64) / 128.0)
+        ang = pos[:, None] * inv[None]
+        cos, sin = torch.cos(ang).float()[None, :, None, :], torch.sin(ang).float()[None, :, None, :]
+        cond = torch.stack([c.float() for c in conds])  # [B, Nc, d]
+        bfr = lambda t: t.bfloat16().float()  # noqa: E731
+        L = cfg.n_layers if layers is None else layers
+        for l in range(L):
+            m = mod + W.ada_table[l][None]
+            sh1, sc1, g1, sh2, sc2, g2 = [m[:, i * d:(i + 1) * d][:, None, :] for i in range(6)]
+            a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc1) + sh1)
+            qkv = bfr(a @ f(W.w_qkv[l]).T)
+            q = qkv[..., :H * hd].reshape(B, N, H, hd)
+            k = qkv[..., H * hd:(H + Hk) * hd].reshape(B, N, Hk, hd)
+            v = qkv[..., (H + Hk) * hd:].reshape(B, N, Hk, hd)
+            q, k = bfr(_rope(q, cos, sin)), bfr(_rope(k, cos, sin))
+            k = k.repeat_interleave(H // Hk, dim=2)
+            v = v.repeat_interleave(H // Hk, dim=2)
+            o = torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                                                 v.transpose(1, 2))
+            o = bfr(o.transpose(1, 2).reshape(B, N, H * hd))
+            h = h + g1 * (o @ f(W.w_o[l]).T)
+            c = bfr(_rmsnorm(h, cfg.norm_eps))
+            qc = bfr(c @ f(W.w_qc[l]).T).reshape(B, N, H, hd)
+            kvc = bfr(cond @ f(W.w_kvc[l]).T)
+            kc = kvc[..., :Hk * hd].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
+            vc = kvc[..., Hk * hd:].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
+            oc = torch.nn.functional.scaled_dot_product_attention(qc.transpose(1, 2), kc.transpose(1, 2),
+                                                                  vc.transpose(1, 2))
+            oc = bfr(oc.transpose(1, 2).reshape(B, N, H * hd))
+            h = h + oc @ f(W.w_oc[l]).T
+            mm = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc2) + sh2)
+            gu = mm @ f(W.w_gu[l]).T
+            gt, up = bfr(gu[..., 0::2]), bfr(gu[..., 1::2])
+            hid = bfr(silu(gt) * up)
+            h = h + g2 * (hid @ f(W.w_down[l]).T)
+        shf, scf = fmod[:, :d][:, None, :], fmod[:, d:][:, None, :]
+        a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + scf) + shf)
+        v = a @ f(W.w_out).T
+        return v.reshape(B, T, C)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+
+
+# ------------------------------------------------- StreamPipeline velocity model --
+@dataclass
+class _Pending:
+    xs: list = field(default_factory=list)
+    ts: list = field(default_factory=list)
+    conds: list = field(default_factory=list)
+
+
+class DiTVelocity:
+    """Velocity-model plug-in for ``StreamPipeline``: the DiT replaces ToyFlowModel.
+
+    Each tick, every active slot contributes one DiT row per condition (+ one
+    unconditional row when its guidance step needs a negative); all rows run in ONE
+    batched forward, each with its own timestep sigma[step] (north_star (a)).  The
+    solver reads the fp32 velocities in place (RF_ROWF_V_F32).
+    """
+
+    def __init__(self, dit: DiT, uncond_prompt: int = 0):
+        self.dit = dit
+        self.uncond_prompt = uncond_prompt
+        self._p = _Pending()
+
+    def _row(self, x, t, prompt_hash) -> int:
+        self._p.xs.append(x)
+        self._p.ts.append(t)
+        self._p.conds.append(self.dit.cond_tokens(prompt_hash))
+        return len(self._p.xs) - 1
+
+    def _ptr(self, idx) -> int:
+        return self.dit.out[idx].data_ptr()
+
+    def prepare_row(self, pipe, slot, row, t_curr: float, need_uncond: bool) -> None:
+        conds = slot.request.conditions
+        if len(self._p.xs) + len(conds) + int(need_uncond) > self.dit.max_rows:
+            raise ValueError("DiT batch exceeds max_rows; raise DiT(max_rows=...)")
+        row.n_cond = len(conds)
+        for j, c in enumerate(conds):
+            row.cond_x0[j] = self._ptr(self._row(slot.x, t_curr, c.prompt_hash))
+            if len(conds) > 1:
+                w = c.weight_device()
+                row.cond_w[j] = None if w is None else w.data_ptr()
+        if need_uncond:
+            row.uncond_x0 = self._ptr(self._row(slot.x, t_curr, self.uncond_prompt))
+        row.flags |= _native.RF_ROWF_COND_V | _native.RF_ROWF_UNCOND_V | _native.RF_ROWF_V_F32
+
+    def forward(self, pipe) -> None:
+        p, self._p = self._p, _Pending()
+        if p.xs:
+            self.dit.forward(p.xs, p.ts, p.conds)

@@ -496,7 +496,10 @@ class StreamPipeline:
                     row.noise_model = nbuf[0].data_ptr()
                     row.jitter_t = jitter * t_curr
             else:
-                self.velocity_model.prepare_row(self, slot, row, t_curr)
+                # the DiT computes every row of the tick in one batched forward (below)
+                need_uncond = (base.guidance_enabled and
+                               guidance_plan(base.rcfg_mode, slot.state, True)[0] == _native.RF_NEG_UNCOND)
+                self.velocity_model.prepare_row(self, slot, row, t_curr, need_uncond)
             curve_pointers(row, lambda n: dev[n])
             if base.guidance_enabled:
                 neg_kind, flags = guidance_plan(base.rcfg_mode, slot.state, True)
@@ -527,7 +530,10 @@ class StreamPipeline:
                     row.noise_step = nbuf[1].data_ptr()
             rows.append(row)
         if self.velocity_model is not None:
-            self.velocity_model.forward(self, slots, rows)
+            ev = self._phase_begin("model")
+            self.velocity_model.forward(self)
+            self._phase_end("model", ev)
+            self.launches_last_tick += getattr(self.velocity_model, "launches_per_forward", 0)
         if draws:
             ev = self._phase_begin("noise")
             fill_normals(draws, self._status)

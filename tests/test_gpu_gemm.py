@@ -1,0 +1,63 @@
+"""tcgen05 GEMM vs a plain PyTorch fp32 reference of the same op (bf16 inputs)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2605_28657_b200 import tensor_ops
+
+    return tensor_ops
+
+
+def ref(a, b):
+    return a.float() @ b.float().T
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 128, 64, 128), (200, 256, 128, 256), (3000, 2048, 2048, 256),
+                                      (3000, 2048, 2048, 128), (1, 256, 64, 256), (517, 384, 640, 128),
+                                      (3000, 12288, 2048, 256)])
+def test_gemm_f32_matches_torch(ops, M, N, K, bn):
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    out = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=bn)
+    r = ref(a, b)
+    err = (out - r).abs().max().item() / r.abs().max().item()
+    assert err < 1e-5, err
+
+
+def test_gemm_bf16_and_scale(ops):
+    a = torch.randn(300, 512, device="cuda").bfloat16()
+    b = torch.randn(256, 512, device="cuda").bfloat16()
+    out = ops.gemm(a, b, epilogue=ops.EPI_BF16)
+    r = ref(a, b)
+    assert ((out.float() - r).abs() <= r.abs() * 2 ** -8 + 1e-2).all()
+    s = ops.gemm(a, b, epilogue=ops.EPI_F32_SCALE, alpha=0.25)
+    assert torch.allclose(s, 0.25 * r, rtol=1e-5, atol=1e-3)
+
+
+def test_gemm_resid_gate(ops):
+    B, T, K, N = 3, 100, 256, 512
+    a = torch.randn(B * T, K, device="cuda").bfloat16()
+    b = torch.randn(N, K, device="cuda").bfloat16()
+    gate = torch.randn(B, N, device="cuda")
+    x0 = torch.randn(B * T, N, device="cuda")
+    x = x0.clone()
+    ops.gemm(a, b, out=x, epilogue=ops.EPI_RESID_GATE, gate=gate, rows_per_batch=T)
+    r = x0 + gate.repeat_interleave(T, 0) * ref(a, b)
+    assert torch.allclose(x, r, rtol=1e-5, atol=1e-3)
+
+
+def test_gemm_swiglu(ops):
+    M, K, H = 260, 256, 384
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    wg = torch.randn(H, K, device="cuda").bfloat16() * 0.1
+    wu = torch.randn(H, K, device="cuda").bfloat16() * 0.1
+    w = torch.stack([wg, wu], 1).reshape(2 * H, K).contiguous()   # interleaved (g, u) rows
+    out = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256)
+    g, u = ref(a, wg).bfloat16().float(), ref(a, wu).bfloat16().float()
+    r = torch.nn.functional.silu(g) * u
+    assert torch.allclose(out.float(), r, rtol=2e-2, atol=2e-2)

@@ -57,6 +57,18 @@ def main():
         print("decode full 60s (us):", timed(lambda: codec.decode_device(lat, 0, 1500, 0, True), a.iters, flush))
         lat240 = torch.randn(6000, 64, dtype=torch.float64, device=dev) * 0.5
         print("decode full 240s (us):", timed(lambda: codec.decode_device(lat240, 0, 6000, 0, True), a.iters, flush))
+    if a.what in ("gemm", "all"):
+        from paper_2605_28657_b200 import tensor_ops as ops
+        for (M, N, K) in ((3000, 4096, 2048), (3000, 2048, 2048), (3000, 12288, 2048), (3000, 2048, 6144),
+                          (6000, 12288, 2048), (8192, 8192, 8192)):
+            A = torch.randn(M, K, device=dev).bfloat16()
+            B = torch.randn(N, K, device=dev).bfloat16()
+            for bn in (128, 256):
+                o = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+                us = timed(lambda: ops.gemm(A, B, out=o, block_n=bn), a.iters, flush)
+                print(f"gemm {M}x{N}x{K} BN={bn}: {us:8.1f} us  {2*M*N*K/us/1e6:7.1f} TFLOP/s")
+            us = timed(lambda: torch.matmul(A, B.T), a.iters, flush)
+            print(f"cublas {M}x{N}x{K}:      {us:8.1f} us  {2*M*N*K/us/1e6:7.1f} TFLOP/s")
     if a.what in ("noise", "all"):
         for nd, n in ((1, 96000), (8, 96000), (16, 96000)):
             outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(nd)]
