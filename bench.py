@@ -1,24 +1,30 @@
 #!/usr/bin/env python
 """Benchmark: decoder completions/s for 60-s music at ring depth 4, S=8 (BASELINE config 2).
 
-A step is one ``StreamPipeline.tick()`` of the ring (T=1500 latent frames at 25 Hz,
-D=64 channels, depth 4, S=8, source present, denoise 1.0); at depth 4 / S=8 the ring
-completes one generation every 2 ticks.  value = completions of all ranks / max-over-
-ranks device time (CUDA events on the pipeline's stream around each tick; L2 flushed
-between ticks outside the timed events).
+A step is one ``StreamPipeline.tick()`` of the ring: T=1500 latent frames (60 s at 25 Hz),
+D=64 channels, depth 4, S=8, source present, denoise 1.0, SDE re-noise solver.  The
+velocity model is the ACE-Step-1.5-shape 24-layer DiT (config 2; ``paper_2605_28657_b200.dit``,
+random init, bf16 operands / fp32 accumulation); every tick runs ONE batched DiT forward
+over the 4 ring rows, each at its own timestep, then the fused solver.  At depth 4 / S=8
+the ring completes one generation every 2 ticks.
+
+  value     = completions of all ranks / max-over-ranks device time (CUDA events on the
+              pipeline stream around each tick; L2 flushed between ticks, outside events)
+  e2e       = the same through the public API with host buffers: per-tick shared-curve
+              write from host memory, every CompletionRecord.latent read back to host
+  toy_path  = the same ring with the reference's own ToyFlowModel as velocity model (the
+              only model the reference has), for the apples-to-apples CPU comparison
+  cpu_baseline / --impl reference = the reference's CPU path (oracle port, float64 numpy)
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun: each rank drives its own independent stream (its own ring,
-seed = rank): weak scaling, no data-path collective.  --impl reference times the
-reference's CPU path (the oracle port oracle/ringflow_np.py, float64 numpy) on the
-host cores, one independent stream per process.
+N > 1 (torchrun): every rank drives its own independent stream (own ring and DiT,
+seed = rank): weak scaling, no data-path collective.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import multiprocessing as mp
 import os
 import subprocess
@@ -40,11 +46,12 @@ L2_FLUSH_BYTES = 256 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
-    ap.add_argument("--warmup", type=int, default=32)
+    ap.add_argument("--steps", type=int, default=32)
+    ap.add_argument("--warmup", type=int, default=12)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-toy", action="store_true")
     return ap.parse_args()
 
 
@@ -52,9 +59,9 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, 1400.0, "fallback"
 
 
 # ------------------------------------------------------------------- clocks -----
@@ -68,6 +75,14 @@ class ClockSampler:
         self.proc = None
         self.path = tempfile.mktemp(suffix=".csv")
 
+    def _query(self):
+        try:
+            return subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                   "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                  timeout=20).stdout
+        except Exception:
+            return ""
+
     def __enter__(self):
         try:
             self.fh = open(self.path, "w")
@@ -80,13 +95,7 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
-            # one synchronous sample at the end so a short timed region still has data
-            try:
-                snap = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                      timeout=20).stdout
-            except Exception:
-                snap = ""
+            snap = self._query()  # at least one sample while the GPU is still busy
             self.proc.terminate()
             self.proc.wait()
             self.fh.close()
@@ -124,10 +133,42 @@ def make_request(rf, stream_id):
     return rf.GenerationRequest(conditions=(cond,))
 
 
-def solve_bytes_per_row():
-    # rf_tick_kernel touches, per element (float64): x read+write, x0 partial, style
-    # offset, model noise, sde noise, source = 7 x 8 B (no curves at config 2).
-    return T * D * 7 * 8
+def solve_bytes_per_row(toy: bool):
+    # rf_tick_kernel, per element: x read + write (f64), source (f64), sde noise (f64);
+    # toy model adds the x0 table, the style offset and the model noise (f64);
+    # the DiT path reads the velocity (f32) instead.
+    return T * D * ((7 * 8) if toy else (4 * 8 + 4))
+
+
+def timed_ticks(pipe, steps, flush, stream):
+    import torch
+
+    pairs, completions, launches = [], 0, 0
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        recs = pipe.tick()
+        b.record(stream)
+        pairs.append((a, b))
+        completions += len(recs)
+        launches += pipe.launches_last_tick
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in pairs), completions, launches
+
+
+def phase_times(pipe, steps, flush, stream):
+    import torch
+
+    phases = pipe.enable_phase_timing(True)
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        pipe.tick()
+    torch.cuda.synchronize()
+    pipe.enable_phase_timing(False)
+    return {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in phases.items()}
 
 
 def run_ours(args):
@@ -136,6 +177,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2605_28657_b200 as rf
+    from paper_2605_28657_b200 import dit as dit_mod
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -144,78 +186,53 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    pipe = rf.StreamPipeline(rf.PipelineConfig(depth=DEPTH, steps=STEPS, frames=T, channels=D, seed=rank),
-                             request=make_request(rf, rank))
-    st = pipe.stream
+    hbm_peak, bf16_burst, bf16_sust, peak_src = peaks()
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    conf = rf.PipelineConfig(depth=DEPTH, steps=STEPS, frames=T, channels=D, seed=rank)
 
-    def flush_l2():
-        with torch.cuda.stream(st):
-            flush.fill_(1)
-
+    # ---------------- config 2: the DiT velocity model ----------------
+    dcfg = dit_mod.DiTConfig()
+    model = dit_mod.DiT(dcfg, frames=T, max_rows=DEPTH)
+    pipe = rf.StreamPipeline(conf, request=make_request(rf, rank), velocity_model=dit_mod.DiTVelocity(model))
+    st = pipe.stream
     for _ in range(args.warmup):
         pipe.tick()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-
-    # ---- device-timed run (kernel-resident inputs) ----
-    pairs, completions, launches = [], 0, 0
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            flush_l2()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(st)
-            recs = pipe.tick()
-            b.record(st)
-            pairs.append((a, b))
-            completions += len(recs)
-            launches += pipe.launches_last_tick
-        torch.cuda.synchronize()
-    dev_ms = sum(a.elapsed_time(b) for a, b in pairs)
+        dev_ms, completions, launches = timed_ticks(pipe, args.steps, flush, st)
     clocks = clk.summary()
-
-    # ---- roofline of the dominant kernel (fused solve) ----
-    phases = pipe.enable_phase_timing(True)
-    for _ in range(args.steps):
-        flush_l2()
-        pipe.tick()
-    torch.cuda.synchronize()
-    pipe.enable_phase_timing(False)
-    phase_ms = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in phases.items()}
-    rows = DEPTH  # steady state: every slot active each tick
-    solve_bytes = rows * solve_bytes_per_row()
-    hbm_peak, _, peak_src = peaks()
-    achieved = solve_bytes / (phase_ms["solve"] * 1e-3) / 1e9
+    phase_ms = phase_times(pipe, max(4, args.steps // 4), flush, st)
+    dit_flops = dcfg.flops_per_forward(DEPTH, T)
+    dit_tflops = dit_flops / (phase_ms["model"] * 1e-3) / 1e12
 
     # ---- end-to-end through the public API with host buffers ----
-    curve_host = torch.from_numpy(np.clip(np.linspace(0.0, 1.0, T), 0, 1)).pin_memory()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    curve = np.linspace(0.0, 1.0, T)
     t0 = time.perf_counter()
     e2e_done, h2d, d2h = 0, 0, 0
     for k in range(args.steps):
-        # per-tick control input from pinned host memory (config 4-style shared write)
-        pipe.set_shared_curve("sde_denoise_curve", 1.0 if k % 2 else 0.999)
+        pipe.set_shared_curve("sde_denoise_curve", curve if k % 2 else 1.0)   # host -> device, [T] f64
         h2d += T * 8
         for r in pipe.tick():
-            _ = r.latent   # device -> host copy of the completion
+            _ = r.latent                                                       # device -> host, [T, D] f64
             d2h += T * D * 8
             e2e_done += 1
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    del curve_host
+    pipe.set_shared_curve("sde_denoise_curve", 1.0)
 
     # ---- windowed decode (3-s window + overlap 15) of the last completion ----
     codec = rf.ToyCodec(channels=D, hop=HOP)
-    lat = pipe._last_emitted  # device float64 [T, D]
+    lat = pipe._last_emitted
     with torch.cuda.stream(st):
-        for _ in range(5):
+        for _ in range(3):
             codec.decode_device(lat, T - WINDOW, T, OVERLAP, False)
         ev = []
-        for _ in range(20):
+        for _ in range(10):
             flush.fill_(1)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
@@ -223,13 +240,33 @@ def run_ours(args):
             b.record(st)
             ev.append((a, b))
     torch.cuda.synchronize()
-    decode_ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+    decode_ms = sorted(a.elapsed_time(b) for a, b in ev)[len(ev) // 2]
+    del pipe, model
+    torch.cuda.empty_cache()
+
+    # ---------------- toy-velocity leg (the reference's own model) ----------------
+    toy = None
+    if not args.no_toy:
+        tp = rf.StreamPipeline(conf, request=make_request(rf, rank))
+        for _ in range(32):
+            tp.tick()
+        torch.cuda.synchronize()
+        t_ms, t_done, t_launch = timed_ticks(tp, 64, flush, tp.stream)
+        t_phase = phase_times(tp, 16, flush, tp.stream)
+        sb = DEPTH * solve_bytes_per_row(True)
+        toy = {"value": round(t_done / (t_ms * 1e-3), 2), "unit": UNIT, "ms_per_step": round(t_ms / 64, 5),
+               "phase_ms": {k: round(v, 5) for k, v in t_phase.items()},
+               "solver_roofline": {"bound": "hbm", "kernel": "rf_tick_kernel",
+                                   "achieved": round(sb / (t_phase["solve"] * 1e-3) / 1e9, 1), "peak": hbm_peak,
+                                   "unit": "GB/s", "frac": round(sb / (t_phase["solve"] * 1e-3) / 1e9 / hbm_peak, 4),
+                                   "algorithmic_bytes_per_launch": sb},
+               "gpu_launches": t_launch, "dtype": "f64",
+               "note": "same ring and solver with ToyFlowModel velocities (bit-exact vs the reference)"}
 
     # ---- aggregate over ranks ----
-    tot = torch.tensor([completions, dev_ms, e2e_done, e2e_s, launches], dtype=torch.float64, device=dev)
+    tot = torch.tensor([completions, dev_ms, e2e_done, e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
-        s = tot.clone()
-        m = tot.clone()
+        s, m = tot.clone(), tot.clone()
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         completions_all, dev_ms_max, e2e_all, e2e_max = s[0].item(), m[1].item(), s[2].item(), m[3].item()
@@ -243,11 +280,14 @@ def run_ours(args):
     value = completions_all / (dev_ms_max * 1e-3)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 5), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config 2: 60-s latent T=1500 x D=64, ring depth 4, S=8, toy velocity model, "
-                               "source present, denoise 1.0; one independent stream per GPU",
+        "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "config 2: ACE-Step-1.5-shape 24-layer DiT (d=2048, 16/8 heads, SwiGLU 6144, "
+                               "random init), 60-s latent T=1500 x D=64, ring depth 4, S=8, source present, "
+                               "denoise 1.0; one independent stream per GPU",
                    "frames": T, "channels": D, "depth": DEPTH, "steps_per_generation": STEPS,
+                   "dit_params": dcfg.params(), "dit_flops_per_tick": dit_flops,
+                   "ring_state": "float64", "dit_compute": "bf16 operands, fp32 accumulate/residual",
                    "l2": "flushed (256 MiB write) between timed ticks, outside the events",
                    "completions_timed": int(completions_all)},
         "e2e": {"value": round(e2e_all / e2e_max, 3), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
@@ -255,13 +295,17 @@ def run_ours(args):
                 "note": "wall clock through StreamPipeline: per-tick shared-curve write from host, "
                         "CompletionRecord.latent read back to host"},
         "windowed_decode_ms": round(decode_ms, 5),
-        "phase_ms": {k: round(v, 5) for k, v in phase_ms.items()},
-        "roofline": {"bound": "hbm", "kernel": "rf_tick_kernel", "achieved": round(achieved, 1), "peak": hbm_peak,
-                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                     "algorithmic_bytes_per_launch": solve_bytes, "peak_source": peak_src},
+        "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+        "roofline": {"bound": "tensor", "kernel": "dit_forward (tcgen05 GEMMs + attention + norms, one launch set)",
+                     "achieved": round(dit_tflops, 1), "peak": bf16_sust, "unit": "TFLOP/s",
+                     "frac": round(dit_tflops / bf16_sust, 4), "traffic": None,
+                     "algorithmic_flops_per_launch": dit_flops,
+                     "peak_source": f"{peak_src} bf16 sustained (burst {bf16_burst})"},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if toy is not None:
+        line["toy_path"] = toy
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, processes=1)
     print(json.dumps(line), flush=True)
@@ -302,9 +346,10 @@ def cpu_baseline(seconds, processes=1):
     ticks = sum(r[1] for r in res)
     wall = max(r[2] for r in res)
     return {"value": round(done / wall, 3), "unit": UNIT, "cores": processes, "kind": "port",
-            "sample": f"oracle/ringflow_np.py StreamPipeline restatement, config 2 (T=1500, D=64, depth 4, S=8), "
-                      f"{processes} independent stream(s), {ticks} warm ticks after {4 * STEPS} warmup, "
-                      f"{wall:.1f} s wall, float64 numpy, 1 thread/process"}
+            "sample": f"oracle/ringflow_np.py StreamPipeline restatement (toy velocity model, the reference's "
+                      f"only model), config-2 shape (T=1500, D=64, depth 4, S=8), {processes} independent "
+                      f"stream(s), {ticks} warm ticks after {4 * STEPS} warmup, {wall:.1f} s wall, float64 numpy, "
+                      f"1 thread/process"}
 
 
 def run_reference(args):
@@ -318,7 +363,7 @@ def run_reference(args):
         "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": "config 2: 60-s latent T=1500 x D=64, ring depth 4, S=8, toy velocity model "
+        "config": {"workload": "config 2 shape: 60-s latent T=1500 x D=64, ring depth 4, S=8, toy velocity model "
                                "(the reference's only model), source present; one stream per host core"},
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -203,14 +203,21 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 } else if constexpr (EPI == kResidGate) {
                     float *o = (float *)epi.out + (int64_t)m * epi.ldo + n;
                     const float *g = epi.gate + (int64_t)(m / epi.rows_per_batch) * epi.gate_ld + n;
+                    // all loads first (out and gate may alias as far as the compiler knows,
+                    // which would otherwise serialise one DRAM round trip per float4)
+                    float4 xv[8], gv[8];
 #pragma unroll
                     for (int v = 0; v < 8; ++v) {
-                        float4 x = *(float4 *)(o + v * 4);
-                        const float4 gg = *(const float4 *)(g + v * 4);
-                        x.x += gg.x * __uint_as_float(r[4 * v]);
-                        x.y += gg.y * __uint_as_float(r[4 * v + 1]);
-                        x.z += gg.z * __uint_as_float(r[4 * v + 2]);
-                        x.w += gg.w * __uint_as_float(r[4 * v + 3]);
+                        xv[v] = __ldcs((const float4 *)(o + v * 4));
+                        gv[v] = __ldg((const float4 *)(g + v * 4));
+                    }
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        float4 x = xv[v];
+                        x.x += gv[v].x * __uint_as_float(r[4 * v]);
+                        x.y += gv[v].y * __uint_as_float(r[4 * v + 1]);
+                        x.z += gv[v].z * __uint_as_float(r[4 * v + 2]);
+                        x.w += gv[v].w * __uint_as_float(r[4 * v + 3]);
                         *(float4 *)(o + v * 4) = x;
                     }
                 } else if constexpr (EPI == kSwiGLU) {

@@ -302,6 +302,8 @@ class DiTVelocity:
         self.dit = dit
         self.uncond_prompt = uncond_prompt
         self._p = _Pending()
+        # kernels per forward (csrc/rf_dit.cu): 9 conditioning + in-proj + 12 per layer + 2 final
+        self.launches_per_forward = 12 + 12 * dit.cfg.n_layers
 
     def _row(self, x, t, prompt_hash) -> int:
         self._p.xs.append(x)

@@ -77,5 +77,25 @@ def main():
             print(f"noise {nd} x {n} (us):", timed(lambda: fill_normals(draws, st), a.iters, flush))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "epi"):
     main()
+
+
+def epilogues():
+    from paper_2605_28657_b200 import tensor_ops as ops
+    dev = torch.device("cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    M, N, K = 3000, 2048, 2048
+    A = torch.randn(M, K, device=dev).bfloat16()
+    B = torch.randn(N, K, device=dev).bfloat16()
+    x = torch.zeros(M, N, device=dev)
+    gate = torch.randn(4, N, device=dev)
+    for name, kw in (("f32", dict(epilogue=ops.EPI_F32, out=x)),
+                     ("resid_gate", dict(epilogue=ops.EPI_RESID_GATE, out=x, gate=gate, rows_per_batch=750)),
+                     ("bf16", dict(epilogue=ops.EPI_BF16))):
+        us = timed(lambda: ops.gemm(A, B, block_n=256, **kw), 10, flush)
+        print(f"epilogue {name}: {us:.1f} us")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "epi":
+    epilogues()
