@@ -201,6 +201,12 @@ int rf_attention_bf16(const void *q, const void *k, const void *v, void *out, in
                       int32_t n_k, int32_t heads, int32_t kv_heads, int64_t ldq, int64_t ldk, int64_t ldv,
                       int64_t ldo, void *stream);
 
+/* Same attention on tcgen05/TMEM (two-pass softmax, O accumulated in TMEM); V is given
+ * transposed: vt [batch, kv_heads, 128, n_k_pad] (keys contiguous, pad columns zero). */
+int rf_attention_tc_bf16(const void *q, const void *k, const void *vt, void *out, int32_t batch, int32_t n_q,
+                         int32_t n_k, int32_t n_k_pad, int32_t heads, int32_t kv_heads, int64_t ldq, int64_t ldk,
+                         int64_t ldo, void *stream);
+
 /* --------------------------------------------------- ACE-Step-shape DiT (A8) ------
  * The velocity model that replaces the reference's ToyFlowModel for BASELINE configs
  * 2-5 (the reference has no DiT: builder-defined ACE-Step-1.5 shape).

@@ -16,6 +16,7 @@
 //   h  += gate_mlp[row] * (SwiGLU(m Wgu^T) Wdown^T)                   GEMM SwiGLU epi, GEMM
 // then  v = (RMSNorm(h) * (1 + scale_f[row]) + shift_f[row]) Wout^T (fp32), unpatchified.
 #include <math.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -137,6 +138,10 @@ struct Dit {
     __nv_bfloat16 *xin, *a, *qkv, *att, *qc, *cond, *kvc, *mlp, *tfeat, *tbuf;
     float *h, *tmp, *mod, *mods, *fmod, *vout;
     float2 *rope;
+    __nv_bfloat16 *vt_self, *vt_cross;    // V^T [rows, Hkv, 128, keys_pad] for the tcgen05 attention
+    int n_pad, nc_pad;
+    AttnPlan a_self, a_cross;
+    bool tc_attention;
     // GEMM plans (tensor maps at max rows)
     GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out;
     std::vector<GemmPlan> p_qkv, p_o, p_qc, p_kvc, p_oc, p_gu, p_down;
@@ -166,6 +171,9 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
     void *h = take(BN * D * 4), *tmp = take(rows_pad * D * 4), *mod = take(rows_pad * 6 * D * 4);
     void *mods = take((int64_t)c.n_layers * max_rows * 6 * D * 4), *fmod = take(rows_pad * 2 * D * 4);
     void *vout = take(BN * in_dim * 4), *rope = take(N * 64 * 8);
+    const int64_t n_pad = (N + 7) / 8 * 8, nc_pad = (c.n_cond_tokens + 7) / 8 * 8;
+    void *vt_self = take((int64_t)max_rows * kv_dim * n_pad * 2);
+    void *vt_cross = take((int64_t)max_rows * kv_dim * nc_pad * 2);
     if (d) {
         d->xin = (__nv_bfloat16 *)xin;
         d->a = (__nv_bfloat16 *)a;
@@ -184,6 +192,10 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
         d->fmod = (float *)fmod;
         d->vout = (float *)vout;
         d->rope = (float2 *)rope;
+        d->vt_self = (__nv_bfloat16 *)vt_self;
+        d->vt_cross = (__nv_bfloat16 *)vt_cross;
+        d->n_pad = (int)n_pad;
+        d->nc_pad = (int)nc_pad;
     }
     return (int64_t)(cur - base);
 }
@@ -238,7 +250,9 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     ws_layout(c, max_rows, frames, d, base);
     const int64_t BN = (int64_t)max_rows * d->tokens, D = c.d_model, L = c.n_layers, Bmax = max_rows;
     const int64_t Bc = (int64_t)max_rows * c.n_cond_tokens;
-    auto bn_for = [](int64_t n) { return n % 256 == 0 ? 256 : 128; };
+    // BN=256 only for wide outputs: at M = 3000 a 128x256 tiling of N <= 2048 leaves the
+    // last wave mostly idle (measured: 2048-wide GEMMs 24 us at BN=128 vs 28 us at 256)
+    auto bn_for = [](int64_t n) { return (n >= 4096 && n % 256 == 0) ? 256 : 128; };
     int rc = 0;
     auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
         if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N));
@@ -273,6 +287,20 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         delete d;
         return rc;
     }
+    if (!rc)
+        rc = attn_plan(&d->a_self, d->qkv, d->qkv_dim, d->q_dim, d->qkv + d->q_dim, d->qkv_dim, d->kv_dim, d->vt_self,
+                       max_rows, d->tokens, d->tokens, d->n_pad, c.n_heads, c.n_kv_heads);
+    if (!rc)
+        rc = attn_plan(&d->a_cross, d->qc, d->q_dim, d->q_dim, d->kvc, 2 * d->kv_dim, d->kv_dim, d->vt_cross, max_rows,
+                       d->tokens, c.n_cond_tokens, d->nc_pad, c.n_heads, c.n_kv_heads);
+    if (rc) {
+        delete d;
+        return rc;
+    }
+    d->tc_attention = getenv("RF_ATTN_MMA_SYNC") == nullptr;   // the tcgen05 kernel is the default
+    // V^T pad columns are never written: zero them once
+    RF_TRY_CUDA(cudaMemsetAsync(d->vt_self, 0, (size_t)max_rows * d->kv_dim * d->n_pad * 2, (cudaStream_t)stream));
+    RF_TRY_CUDA(cudaMemsetAsync(d->vt_cross, 0, (size_t)max_rows * d->kv_dim * d->nc_pad * 2, (cudaStream_t)stream));
     rf_dit_rope_table<<<d->tokens, 64, 0, (cudaStream_t)stream>>>(d->rope, d->tokens, c.rope_theta);
     RF_TRY_LAUNCH("rf_dit_rope_table");
     *handle = d;
@@ -343,15 +371,24 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
         const float *md = d.mods + l * B * W6;  // [B][6][D]: shift,scale,gate (msa), shift,scale,gate (mlp)
         // self-attention
         RF_TRY(norm_mod(d, d.h, M, md + 0 * D, md + 1 * D, W6, d.a, st));
+        const VtOut vts{d.vt_self, (int)(d.q_dim + d.kv_dim), c.n_kv_heads, d.n_pad};
         RF_TRY(gemm_run(d.p_qkv[l], 5 /* bf16 + RoPE */, d.qkv, d.qkv_dim, nullptr, 0, (int)N, 1.f, st, d.rope,
-                        (int)(d.q_dim + d.kv_dim), M));
-        RF_TRY(rf_attention_bf16(d.qkv, d.qkv + d.q_dim, d.qkv + d.q_dim + d.kv_dim, d.att, (int)B, (int)N,
-                                 (int)N, c.n_heads, c.n_kv_heads, d.qkv_dim, d.qkv_dim, d.qkv_dim, d.q_dim, st));
+                        (int)(d.q_dim + d.kv_dim), M, d.tc_attention ? &vts : nullptr));
+        if (d.tc_attention)
+            RF_TRY(attn_run(d.a_self, d.att, d.q_dim, (int)B, st));
+        else
+            RF_TRY(rf_attention_bf16(d.qkv, d.qkv + d.q_dim, d.qkv + d.q_dim + d.kv_dim, d.att, (int)B, (int)N,
+                                     (int)N, c.n_heads, c.n_kv_heads, d.qkv_dim, d.qkv_dim, d.qkv_dim, d.q_dim, st));
         RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
         // cross-attention to the row's conditioning tokens (residual, no gate)
         RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
         RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
-        RF_TRY(gemm_run(d.p_kvc[l], RF_EPI_BF16, d.kvc, 2 * d.kv_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, B * Nc));
+        const VtOut vtc{d.vt_cross, (int)d.kv_dim, c.n_kv_heads, d.nc_pad};
+        RF_TRY(gemm_run(d.p_kvc[l], 5 /* bf16, V^T out */, d.kvc, 2 * d.kv_dim, nullptr, 0, (int)Nc, 1.f, st, d.rope, 0,
+                        B * Nc, d.tc_attention ? &vtc : nullptr));
+        if (d.tc_attention)
+            RF_TRY(attn_run(d.a_cross, d.att, d.q_dim, (int)B, st));
+        else
         RF_TRY(rf_attention_bf16(d.qc, d.kvc, d.kvc + d.kv_dim, d.att, (int)B, (int)N, (int)Nc, c.n_heads,
                                  c.n_kv_heads, d.q_dim, 2 * d.kv_dim, 2 * d.kv_dim, d.q_dim, st));
         RF_TRY(gemm_run(d.p_oc[l], RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));

@@ -78,11 +78,14 @@ int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, i
 }
 
 int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,
-             int rows_per_batch, float alpha, cudaStream_t st, const float2 *rope, int rope_cols, int64_t M) {
+             int rows_per_batch, float alpha, cudaStream_t st, const float2 *rope, int rope_cols, int64_t M,
+             const VtOut *vt) {
     // The tensor maps cover the plan's (maximum) M; a smaller M only shortens the tile walk.
     GemmPlan p = plan;
     if (M > 0 && M < p.M) p.M = M;
-    gemm::EpiArgs e{out, ldo, gate, gate_ld, rows_per_batch > 0 ? rows_per_batch : 1, alpha, rope, rope_cols};
+    gemm::EpiArgs e{out, ldo, gate, gate_ld, rows_per_batch > 0 ? rows_per_batch : 1, alpha, rope, rope_cols,
+                    vt ? (__nv_bfloat16 *)vt->ptr : nullptr, vt ? vt->col0 : 0, vt ? vt->heads : 0,
+                    vt ? vt->ld : 0};
     if (p.bn == 256) {
         switch (epi) {
             case gemm::kStoreBF16: return launch<256, gemm::kStoreBF16>(p, e, st);

@@ -34,6 +34,12 @@ struct EpiArgs {
     float alpha;
     const float2 *rope;     // kBF16Rope: (cos, sin)[pos * 64 + pair], pos = m % rows_per_batch
     int rope_cols;
+    // kBF16Rope: columns >= vt_col0 (the V heads) are written transposed instead, to
+    // vt[((b * vt_heads + hv) * 128 + dim) * vt_ld + pos] (b = m / rows_per_batch) -- the
+    // K-major B operand of the attention's P V^T product.
+    __nv_bfloat16 *vt;
+    int vt_col0, vt_heads;
+    int64_t vt_ld;
 };
 
 constexpr int BM = 128, BK = 64;
@@ -168,6 +174,15 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         *(uint4 *)(o + v * 8) = pk;
                     }
                 } else if constexpr (EPI == kBF16Rope) {
+                    if (epi.vt && n >= epi.vt_col0) {
+                        const int cv = n - epi.vt_col0, hv = cv >> 7, dim0 = cv & 127;
+                        const int64_t b = m / epi.rows_per_batch, pos = m % epi.rows_per_batch;
+                        __nv_bfloat16 *dst = epi.vt + ((b * epi.vt_heads + hv) * 128 + dim0) * epi.vt_ld + pos;
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)   // lanes hold consecutive tokens: coalesced
+                            dst[(int64_t)e * epi.vt_ld] = __float2bfloat16(__uint_as_float(r[e]));
+                        continue;
+                    }
                     __nv_bfloat16 *o = (__nv_bfloat16 *)epi.out + (int64_t)m * epi.ldo + n;
                     const bool rot = n < epi.rope_cols;
                     const float2 *cs = epi.rope + (int64_t)(m % epi.rows_per_batch) * 64 + ((n & 127) >> 1);
