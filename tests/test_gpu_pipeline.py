@@ -51,15 +51,21 @@ def test_scenario_matches_reference(rf, goldens, name):
     assert np.array_equal(r_gpu[ok] == 0.0, r_ref[ok] == 0.0)
 
 
-def _c2_spec(depth, steps, ticks, frames=1500, channels=64, **req):
+def _c2_spec(depth, steps, ticks, frames=1500, channels=64, extra_ops=(), **req):
     return dict(config=dict(depth=depth, steps=steps, frames=frames, channels=channels),
-                request=dict(prompt="bench prompt", source="src", **req), ops=[("tick", ticks)])
+                request=dict(prompt="bench prompt", source="src", **req), ops=[("tick", ticks), *extra_ops])
 
 
 @pytest.mark.parametrize("spec", [
     _c2_spec(4, 8, 24),                                       # BASELINE config 2 shape
     _c2_spec(8, 8, 20),                                       # config 3 depth
     _c2_spec(4, 8, 20, sde="ramp"),                           # config 4 per-frame blend
+    # config 3 exactly: depth 8, S=8, the 60-value continuous denoise sweep (one
+    # set_denoise per tick -> per-slot heterogeneous schedules across the ring)
+    _c2_spec(8, 8, 8, extra_ops=[("sweep", 60)]),
+    # config 4 exactly: per-frame source blend (sde curve linspace(0,1,T)) and a shared
+    # sde_denoise_curve write every tick (next-tick visibility, no ring drain)
+    _c2_spec(4, 8, 8, sde="ramp", extra_ops=[("modulate", 24)]),
 ])
 def test_full_size_vs_oracle(rf, spec):
     gpu = scenarios.drive(rf, spec)
