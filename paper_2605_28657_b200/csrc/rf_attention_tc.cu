@@ -11,6 +11,8 @@
 //           (K-major; written transposed by the QKV GEMM epilogue), row sums in registers.
 //           With the final max known, O never needs rescaling; O / l at the end.
 // K tiles are double-buffered (the TMA for tile j+1 is in flight while tile j computes).
+#include <stdlib.h>
+
 #include "rf_common.cuh"
 #include "rf_gemm_host.h"
 #include "rf_sm100.cuh"
@@ -253,6 +255,267 @@ rf_attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     if (warp == 0) tmem_dealloc<256 * NH>(tmem);
 }
 
+// ---------------------------------------------------------------------------------
+// Single-pass attention with head ping-pong (the default).
+//
+// CTA = one 128-row query tile x NH query heads sharing a KV head.  Warps 0..4NH-1 run
+// the softmax (warp w: head w / 4, TMEM lane quarter w % 4, one query row per thread);
+// warp 4NH issues the MMAs (one elected thread), warp 4NH+1 issues the TMA loads.
+// Per head a and key tile j:  S_a = Q_a K_j^T (SS MMA into TMEM) -> softmax threads read S,
+// keep a running row max m with LAZY rescaling (O and l are rescaled only when the tile
+// max exceeds m by more than 2^8, so P <= 256 stays exact in bf16/fp32), write
+// P = exp2(S*scale - m) as bf16 into the same TMEM columns -> O_a += P V_j (TS MMA: A from
+// TMEM, V^T from shared memory).  The MMA thread issues PV_a(j), then S_a(j+1), then the
+// other head's pair, so head 1's softmax overlaps head 0's MMAs and vice versa.
+// K and V^T are double-buffered; one pass over the keys (no recomputed S).
+// TMEM: per head S/P 128 columns + O 128 columns (512 for NH = 2).
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <int NH>
+constexpr size_t fa_smem() {
+    return 1024 + (size_t)(NH + 2 + 2) * kOperand + 256;
+}
+
+// debugging timeline ([cta][event][16] u64 clock64), set by rf_attn_set_trace; null in production
+__device__ unsigned long long *g_attn_trace = nullptr;
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define FA_GTRACE(ev)                                                                                     \
+    do {                                                                                                  \
+        if (g_attn_trace)                                                                                 \
+            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ev)) * 16 + 15] = globaltimer(); \
+    } while (0)
+#define FA_TRACE(ev, j)                                                                                  \
+    do {                                                                                                 \
+        if (g_attn_trace && (j) < 16)                                                                    \
+            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ev)) * 16 + (j)] = clock64(); \
+    } while (0)
+
+template <int NH>
+__global__ void __launch_bounds__(128 * NH + 64, 1)
+rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                  const __grid_constant__ CUtensorMap tvt, __nv_bfloat16 *__restrict__ out, int64_t ldo, int Nq,
+                  int Nk, int H, int Hkv, float scale_log2) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sQ = base;                 // [NH]
+    uint8_t *sK = sQ + NH * kOperand;   // [2]
+    uint8_t *sV = sK + 2 * kOperand;    // [2] V^T tiles (rows = head dims, K-major over keys)
+    uint64_t *bar = (uint64_t *)(sV + 2 * kOperand);
+    uint64_t *qfull = bar, *kfull = bar + 1, *kempty = bar + 3, *vfull = bar + 5, *vempty = bar + 7;
+    uint64_t *sfull = bar + 9, *pfull = bar + 11, *odone = bar + 13;
+    uint32_t *tmem_slot = (uint32_t *)(bar + 16);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int MMA_WARP = 4 * NH, TMA_WARP = 4 * NH + 1;
+    if (tid == 0) FA_GTRACE(0);
+    const int group = H / Hkv;
+    const int bh = blockIdx.y, per_b = H / NH, b = bh / per_b, h0 = (bh % per_b) * NH;
+    const int hk = h0 / group;
+    const int q0 = blockIdx.x * kTcRows;
+    const int nt = (Nk + kTcRows - 1) / kTcRows;
+    constexpr uint32_t idesc = idesc_bf16(128, 128);
+
+    if (tid == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tk);
+        tma_prefetch(&tvt);
+        mbar_init(qfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kfull[i], 1);
+            mbar_init(&kempty[i], 1);
+            mbar_init(&vfull[i], 1);
+            mbar_init(&vempty[i], 1);
+            mbar_init(&sfull[i], 1);
+            mbar_init(&pfull[i], 4);   // the 4 softmax warps of the head
+            mbar_init(&odone[i], 1);
+        }
+        mbar_fence_init();
+    }
+    if (warp == MMA_WARP) tmem_alloc<256 * NH>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == TMA_WARP) {
+        if (elect_one()) {
+            mbar_expect_tx(qfull, NH * kOperand);
+            for (int a = 0; a < NH; ++a) {
+                tma_load_2d(sQ + a * kOperand, &tq, qfull, (h0 + a) * 128, b * Nq + q0);
+                tma_load_2d(sQ + a * kOperand + kTile, &tq, qfull, (h0 + a) * 128 + 64, b * Nq + q0);
+            }
+            for (int j = 0; j < nt; ++j) {
+                const int s = j & 1;
+                const uint32_t ph = ((j >> 1) & 1) ^ 1;
+                mbar_wait(&kempty[s], ph);
+                mbar_expect_tx(&kfull[s], kOperand);
+                tma_load_2d(sK + s * kOperand, &tk, &kfull[s], hk * 128, b * Nk + j * 128);
+                tma_load_2d(sK + s * kOperand + kTile, &tk, &kfull[s], hk * 128 + 64, b * Nk + j * 128);
+                mbar_wait(&vempty[s], ph);
+                mbar_expect_tx(&vfull[s], kOperand);
+                tma_load_2d(sV + s * kOperand, &tvt, &vfull[s], j * 128, (b * Hkv + hk) * 128);
+                tma_load_2d(sV + s * kOperand + kTile, &tvt, &vfull[s], j * 128 + 64, (b * Hkv + hk) * 128);
+            }
+        }
+    } else if (warp == MMA_WARP) {
+        if (elect_one()) {
+            auto mma_s = [&](int a, int s) {   // S_a = Q_a K_s^T
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t ad = sdesc_sw128(sQ + a * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
+                    const uint64_t bd = sdesc_sw128(sK + s * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
+                    umma_bf16(tmem + a * 128, ad, bd, idesc, ks > 0);
+                }
+                umma_commit(&sfull[a]);
+            };
+            auto mma_o = [&](int a, int s, bool acc) {   // O_a += P_a V_s (P_a in TMEM over S_a)
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t bd = sdesc_sw128(sV + s * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
+                    umma_bf16_ts(tmem + NH * 128 + a * 128, tmem + a * 128 + ks * 8, bd, idesc,
+                                 (acc || ks > 0) ? 1u : 0u);
+                }
+                umma_commit(&odone[a]);
+            };
+            mbar_wait(qfull, 0);
+            mbar_wait(&kfull[0], 0);
+            tc_fence_after();
+            for (int a = 0; a < NH; ++a) mma_s(a, 0);
+            umma_commit(&kempty[0]);
+            for (int j = 0; j < nt; ++j) {
+                const int s = j & 1, s1 = (j + 1) & 1;
+                for (int a = 0; a < NH; ++a) {
+                    mbar_wait(&pfull[a], j & 1);
+                    if (a == 0) mbar_wait(&vfull[s], (j >> 1) & 1);
+                    tc_fence_after();
+                    FA_TRACE(a, j);
+                    mma_o(a, s, j > 0);
+                    if (a == NH - 1) umma_commit(&vempty[s]);
+                    if (j + 1 < nt) {
+                        // no wait for PV_a(j): tcgen05.mma executes in issue order, so S_a(j+1)
+                        // cannot overwrite the P_a(j) columns before PV_a(j) has read them
+                        if (a == 0) mbar_wait(&kfull[s1], ((j + 1) >> 1) & 1);
+                        tc_fence_after();
+                        FA_TRACE(2 + a, j + 1);
+                        mma_s(a, s1);
+                        if (a == NH - 1) umma_commit(&kempty[s1]);
+                    }
+                }
+            }
+        }
+    } else {
+        // softmax warps: thread owns query row `row` of head a
+        const int a = warp >> 2, quarter = warp & 3;
+        const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+        const uint32_t tS = tmem + lane_base + a * 128, tO = tmem + lane_base + NH * 128 + a * 128;
+        float m = 0.f, l = 0.f;
+        for (int j = 0; j < nt; ++j) {
+            mbar_wait(&sfull[a], j & 1);
+            tc_fence_after();
+            if (quarter == 0 && lane == 0) FA_TRACE(4 + a, j);
+            const int valid = Nk - j * 128;
+            uint32_t r[128];   // the whole S row of this thread (one TMEM pass)
+            tmem_ld32(tS, *(uint32_t(*)[32])(r));
+            tmem_ld32(tS + 32, *(uint32_t(*)[32])(r + 32));
+            tmem_ld32(tS + 64, *(uint32_t(*)[32])(r + 64));
+            tmem_ld32(tS + 96, *(uint32_t(*)[32])(r + 96));
+            tmem_ld_wait();
+            if (valid < 128) {   // the last key tile: keys >= valid are masked
+#pragma unroll
+                for (int e = 0; e < 128; ++e)
+                    if (e >= valid) r[e] = __float_as_uint(-INFINITY);
+            }
+            float tmax = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < 128; e += 2) tmax = fmaxf(tmax, fmaxf(__uint_as_float(r[e]), __uint_as_float(r[e + 1])));
+            tmax *= scale_log2;
+            if (j == 0) {
+                m = tmax;
+            } else {
+                const bool need = tmax > m + 8.f;
+                if (__any_sync(0xffffffffu, need)) {   // lazy rescale of O and l (warp-uniform TMEM traffic)
+                    const float mn = need ? tmax : m;
+                    const float f = ex2_approx(m - mn);
+                    l *= f;
+                    m = mn;
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                        tmem_st32(tO + c * 32, o);
+                    }
+                    tmem_st_wait();
+                }
+            }
+            // P = exp2(S * scale - m) as bf16 pairs into the first 64 columns of S (the row is
+            // in registers).  Arguments are <= 8 (lazy max) or -inf (masked): the MUFU ex2
+            // needs no range fix-up.  l sums the fp32 values (the bf16 rounding of P is below
+            // the output's own bf16 step).
+            const float nm = -m;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pk[16];
+                float ls = 0.f;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const float p0 = ex2_approx(fmaf(__uint_as_float(r[c * 32 + 2 * e]), scale_log2, nm));
+                    const float p1 = ex2_approx(fmaf(__uint_as_float(r[c * 32 + 2 * e + 1]), scale_log2, nm));
+                    ls += p0 + p1;
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
+                    pk[e] = *(uint32_t *)&hh;
+                }
+                l += ls;
+                tmem_st16(tS + c * 16, pk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[a]);
+            if (quarter == 0 && lane == 0) FA_TRACE(6 + a, j);
+        }
+        mbar_wait(&odone[a], (nt - 1) & 1);
+        tc_fence_after();
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        const int qrow = q0 + quarter * 32 + lane;
+        const int h = h0 + a;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tO + c * 32, r);
+            tmem_ld_wait();
+            if (qrow < Nq) {
+                __nv_bfloat16 *dst = out + ((int64_t)b * Nq + qrow) * ldo + h * 128 + c * 32;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]) * inv_l,
+                                                                  __uint_as_float(r[q * 8 + 2 * e + 1]) * inv_l);
+                        w[e] = *(uint32_t *)&hh;
+                    }
+                    *(uint4 *)(dst + q * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) FA_GTRACE(1);
+    if (warp == MMA_WARP) tmem_dealloc<256 * NH>(tmem);
+}
+
 int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const void *k, int64_t ldk, int64_t k_cols,
               const void *vt, int B, int Nq, int Nk, int Nk_pad, int H, int Hkv) {
     if (H % Hkv || Nk_pad % 8 || Nk > Nk_pad) {
@@ -272,9 +535,26 @@ int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const voi
     return rc;
 }
 
+template <int NH>
+static int launch_fa(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fa_smem<NH>()));
+        attr = true;
+    }
+    dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / NH);
+    rf_attn_fa_kernel<NH><<<grid, 128 * NH + 64, fa_smem<NH>(), st>>>(p.tq, p.tk, p.tvt, (__nv_bfloat16 *)out, ldo,
+                                                                     p.Nq, p.Nk, p.H, p.Hkv, sc);
+    RF_TRY_LAUNCH("rf_attn_fa_kernel");
+    return RF_OK;
+}
+
 int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) {
     const bool pair = (p.H / p.Hkv) % 2 == 0;   // two query heads share each KV head
     const float sc = 1.4426950408889634f / sqrtf(128.f);
+    static const bool two_pass = getenv("RF_ATTN_TWO_PASS") != nullptr;   // the earlier two-pass kernel
+    if (!two_pass) return pair ? launch_fa<2>(p, out, ldo, B, sc, st) : launch_fa<1>(p, out, ldo, B, sc, st);
     if (pair) {
         static bool attr = false;
         if (!attr) {
@@ -303,6 +583,13 @@ int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) 
 }  // namespace rf
 
 using namespace rf;
+
+// Debugging aid (not part of the product ABI): per-CTA clock64 timeline of the single-pass
+// attention ([cta][8 events][16 tiles] u64) -- see tools/attn_trace.py.
+extern "C" int rf_attn_set_trace(void *buf) {
+    unsigned long long *p = (unsigned long long *)buf;
+    return cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)) == cudaSuccess ? RF_OK : RF_ECUDA;
+}
 
 extern "C" int rf_attention_tc_bf16(const void *q, const void *k, const void *vt, void *out, int32_t batch,
                                     int32_t n_q, int32_t n_k, int32_t n_k_pad, int32_t heads, int32_t kv_heads,

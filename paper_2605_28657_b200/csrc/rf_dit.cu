@@ -138,13 +138,16 @@ struct Dit {
     __nv_bfloat16 *xin, *a, *qkv, *att, *qc, *cond, *kvc, *mlp, *tfeat, *tbuf;
     float *h, *tmp, *mod, *mods, *fmod, *vout;
     float2 *rope;
-    __nv_bfloat16 *vt_self, *vt_cross;    // V^T [rows, Hkv, 128, keys_pad] for the tcgen05 attention
+    // V^T [rows, Hkv, 128, keys_pad] for the tcgen05 attention (cross: one block per layer)
+    __nv_bfloat16 *vt_self, *vt_cross;
     int n_pad, nc_pad;
-    AttnPlan a_self, a_cross;
+    int64_t vt_cross_layer;                // elements per layer block of vt_cross
+    AttnPlan a_self;
+    std::vector<AttnPlan> a_cross;
     bool tc_attention;
     // GEMM plans (tensor maps at max rows)
-    GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out;
-    std::vector<GemmPlan> p_qkv, p_o, p_qc, p_kvc, p_oc, p_gu, p_down;
+    GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out, p_kvc;
+    std::vector<GemmPlan> p_qkv, p_o, p_qc, p_oc, p_gu, p_down;
 };
 
 static size_t carve(char *&cur, size_t bytes) {
@@ -165,7 +168,8 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
     void *xin = take(BN * in_dim * 2), *a = take(BN * D * 2), *qkv = take(BN * qkv_dim * 2);
     void *att = take(BN * q_dim * 2), *qc = take(BN * q_dim * 2);
     void *cond = take((int64_t)max_rows * c.n_cond_tokens * D * 2);
-    void *kvc = take((int64_t)max_rows * c.n_cond_tokens * 2 * kv_dim * 2);
+    // cross-attention K/V of every layer at once: [rows * n_cond, layers * 2 * kv_dim]
+    void *kvc = take((int64_t)max_rows * c.n_cond_tokens * c.n_layers * 2 * kv_dim * 2);
     void *mlp = take(BN * c.mlp_hidden * 2);
     void *tfeat = take(rows_pad * c.freq_dim * 2), *tbuf = take(rows_pad * D * 2);
     void *h = take(BN * D * 4), *tmp = take(rows_pad * D * 4), *mod = take(rows_pad * 6 * D * 4);
@@ -173,7 +177,7 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
     void *vout = take(BN * in_dim * 4), *rope = take(N * 64 * 8);
     const int64_t n_pad = (N + 7) / 8 * 8, nc_pad = (c.n_cond_tokens + 7) / 8 * 8;
     void *vt_self = take((int64_t)max_rows * kv_dim * n_pad * 2);
-    void *vt_cross = take((int64_t)max_rows * kv_dim * nc_pad * 2);
+    void *vt_cross = take((int64_t)c.n_layers * max_rows * kv_dim * nc_pad * 2);
     if (d) {
         d->xin = (__nv_bfloat16 *)xin;
         d->a = (__nv_bfloat16 *)a;
@@ -196,6 +200,7 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
         d->vt_cross = (__nv_bfloat16 *)vt_cross;
         d->n_pad = (int)n_pad;
         d->nc_pad = (int)nc_pad;
+        d->vt_cross_layer = (int64_t)max_rows * kv_dim * nc_pad;
     }
     return (int64_t)(cur - base);
 }
@@ -250,12 +255,14 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     ws_layout(c, max_rows, frames, d, base);
     const int64_t BN = (int64_t)max_rows * d->tokens, D = c.d_model, L = c.n_layers, Bmax = max_rows;
     const int64_t Bc = (int64_t)max_rows * c.n_cond_tokens;
-    // BN=256 only for wide outputs: at M = 3000 a 128x256 tiling of N <= 2048 leaves the
-    // last wave mostly idle (measured: 2048-wide GEMMs 24 us at BN=128 vs 28 us at 256)
+    // Tile shape per GEMM (tools/gemm_bench.py on B200, M = 3000): 256 x 256 tiles on CTA
+    // pairs (cta_group::2) for wide outputs (N >= 4096); 256 x 128 pair tiles for N = 2048,
+    // where 256-wide tiles leave the second wave mostly idle; single-CTA 128 x 128 tiles
+    // when M is small (the cross-attention K/V of 128 tokens per row).
     auto bn_for = [](int64_t n) { return (n >= 4096 && n % 256 == 0) ? 256 : 128; };
     int rc = 0;
     auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
-        if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N));
+        if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N), M >= 1024 ? 2 : 1);
     };
     plan(&d->p_in, d->xin, w->w_in, BN, D, d->in_dim);
     plan(&d->p_t1, d->tfeat, w->w_t1, Bmax, D, c.freq_dim);
@@ -266,7 +273,6 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     d->p_qkv.resize(L);
     d->p_o.resize(L);
     d->p_qc.resize(L);
-    d->p_kvc.resize(L);
     d->p_oc.resize(L);
     d->p_gu.resize(L);
     d->p_down.resize(L);
@@ -278,11 +284,16 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
         plan(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_qc[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D);
-        plan(&d->p_kvc[l], d->cond, wkvc + l * 2 * d->kv_dim * D, Bc, 2 * d->kv_dim, D);
         plan(&d->p_oc[l], d->att, woc + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_gu[l], d->a, wgu + l * 2 * (int64_t)c.mlp_hidden * D, BN, 2 * (int64_t)c.mlp_hidden, D);
         plan(&d->p_down[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, BN, D, c.mlp_hidden);
+        // gated-residual outputs all update h: bind it once (TMA map of the epilogue)
+        for (GemmPlan *g : {&d->p_o[l], &d->p_oc[l], &d->p_down[l]})
+            if (!rc && g->bn == 128) rc = gemm_plan_c(g, d->h, D);
     }
+    // the cross-attention K/V projections of all layers read the same conditioning tokens:
+    // one [rows * n_cond, L * 2 * kv_dim] GEMM per forward instead of L narrow ones
+    plan(&d->p_kvc, d->cond, wkvc, Bc, L * 2 * d->kv_dim, D);
     if (rc) {
         delete d;
         return rc;
@@ -290,9 +301,11 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     if (!rc)
         rc = attn_plan(&d->a_self, d->qkv, d->qkv_dim, d->q_dim, d->qkv + d->q_dim, d->qkv_dim, d->kv_dim, d->vt_self,
                        max_rows, d->tokens, d->tokens, d->n_pad, c.n_heads, c.n_kv_heads);
-    if (!rc)
-        rc = attn_plan(&d->a_cross, d->qc, d->q_dim, d->q_dim, d->kvc, 2 * d->kv_dim, d->kv_dim, d->vt_cross, max_rows,
-                       d->tokens, c.n_cond_tokens, d->nc_pad, c.n_heads, c.n_kv_heads);
+    d->a_cross.resize(L);
+    for (int64_t l = 0; l < L && !rc; ++l)
+        rc = attn_plan(&d->a_cross[l], d->qc, d->q_dim, d->q_dim, d->kvc + l * 2 * d->kv_dim, L * 2 * d->kv_dim,
+                       d->kv_dim, d->vt_cross + l * d->vt_cross_layer, max_rows, d->tokens, c.n_cond_tokens,
+                       d->nc_pad, c.n_heads, c.n_kv_heads);
     if (rc) {
         delete d;
         return rc;
@@ -300,7 +313,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     d->tc_attention = getenv("RF_ATTN_MMA_SYNC") == nullptr;   // the tcgen05 kernel is the default
     // V^T pad columns are never written: zero them once
     RF_TRY_CUDA(cudaMemsetAsync(d->vt_self, 0, (size_t)max_rows * d->kv_dim * d->n_pad * 2, (cudaStream_t)stream));
-    RF_TRY_CUDA(cudaMemsetAsync(d->vt_cross, 0, (size_t)max_rows * d->kv_dim * d->nc_pad * 2, (cudaStream_t)stream));
+    RF_TRY_CUDA(cudaMemsetAsync(d->vt_cross, 0, (size_t)L * d->vt_cross_layer * 2, (cudaStream_t)stream));
     rf_dit_rope_table<<<d->tokens, 64, 0, (cudaStream_t)stream>>>(d->rope, d->tokens, c.rope_theta);
     RF_TRY_LAUNCH("rf_dit_rope_table");
     *handle = d;
@@ -365,6 +378,12 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
     for (int b = 0; b < rows; ++b)
         RF_TRY_CUDA(cudaMemcpyAsync(d.cond + (int64_t)b * Nc * D, cond_rows[b], Nc * D * 2,
                                     cudaMemcpyDeviceToDevice, st));
+    // cross-attention K (and V^T for the tcgen05 attention) of every layer, one GEMM
+    {
+        const VtOut vtc{d.vt_cross, (int)d.kv_dim, c.n_kv_heads, d.nc_pad, (int)(2 * d.kv_dim), d.vt_cross_layer};
+        RF_TRY(gemm_run(d.p_kvc, 5 /* bf16, V^T out */, d.kvc, L * 2 * d.kv_dim, nullptr, 0, (int)Nc, 1.f, st,
+                        d.rope, 0, B * Nc, d.tc_attention ? &vtc : nullptr));
+    }
     // h = in_proj(patches)
     RF_TRY(gemm_run(d.p_in, RF_EPI_F32, d.h, D, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
     for (int64_t l = 0; l < L; ++l) {
@@ -383,14 +402,12 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
         // cross-attention to the row's conditioning tokens (residual, no gate)
         RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
         RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
-        const VtOut vtc{d.vt_cross, (int)d.kv_dim, c.n_kv_heads, d.nc_pad};
-        RF_TRY(gemm_run(d.p_kvc[l], 5 /* bf16, V^T out */, d.kvc, 2 * d.kv_dim, nullptr, 0, (int)Nc, 1.f, st, d.rope, 0,
-                        B * Nc, d.tc_attention ? &vtc : nullptr));
+        const __nv_bfloat16 *kvl = d.kvc + l * 2 * d.kv_dim;
         if (d.tc_attention)
-            RF_TRY(attn_run(d.a_cross, d.att, d.q_dim, (int)B, st));
+            RF_TRY(attn_run(d.a_cross[l], d.att, d.q_dim, (int)B, st));
         else
-        RF_TRY(rf_attention_bf16(d.qc, d.kvc, d.kvc + d.kv_dim, d.att, (int)B, (int)N, (int)Nc, c.n_heads,
-                                 c.n_kv_heads, d.q_dim, 2 * d.kv_dim, 2 * d.kv_dim, d.q_dim, st));
+            RF_TRY(rf_attention_bf16(d.qc, kvl, kvl + d.kv_dim, d.att, (int)B, (int)N, (int)Nc, c.n_heads,
+                                     c.n_kv_heads, d.q_dim, L * 2 * d.kv_dim, L * 2 * d.kv_dim, d.q_dim, st));
         RF_TRY(gemm_run(d.p_oc[l], RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));
         // SwiGLU MLP
         RF_TRY(norm_mod(d, d.h, M, md + 3 * D, md + 4 * D, W6, d.a, st));

@@ -22,8 +22,21 @@ static PFN_tmapEncodeTiled encode_fn() {
     return fn;
 }
 
+static int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dt, const void *ptr, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+
 int make_tmap_bf16_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                       uint32_t box_inner, uint32_t box_outer) {
+    return make_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, ptr, inner, outer, row_bytes, box_inner, box_outer);
+}
+
+int make_tmap_f32_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                     uint32_t box_inner, uint32_t box_outer) {
+    return make_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, ptr, inner, outer, row_bytes, box_inner, box_outer);
+}
+
+static int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dt, const void *ptr, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
     PFN_tmapEncodeTiled enc = encode_fn();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable");
@@ -33,7 +46,7 @@ int make_tmap_bf16_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_
     cuuint64_t strides[1] = {row_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+    CUresult r = enc(map, dt, 2, const_cast<void *>(ptr), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -44,37 +57,74 @@ int make_tmap_bf16_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_
     return RF_OK;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
-    using C = gemm::Cfg<BN>;
-    auto kern = gemm::rf_gemm_kernel<BN, EPI>;
+    using C = gemm::Cfg<BN, CG, EPI>;
+    auto kern = gemm::rf_gemm_kernel<BN, EPI, CG>;
     static bool attr = false;
     if (!attr) {
         RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         attr = true;
     }
-    const int tiles = (int)((p.M + gemm::BM - 1) / gemm::BM) * (int)(p.N / BN);
-    int grid = sm_count();
-    if (tiles < grid) grid = tiles;
-    kern<<<grid, 192, C::SMEM, st>>>(p.ta, p.tb, (int)p.M, (int)p.N, (int)p.K, e);
+    const int tiles = (int)((p.M + gemm::BM * CG - 1) / (gemm::BM * CG)) * (int)(p.N / BN);
+    int units = sm_count() / CG;   // persistent: one CTA (pair) per SM (pair)
+    if (tiles < units) units = tiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(units * CG));
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = CG == 2 ? 1 : 0;
+    RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, (int)p.M, (int)p.N, (int)p.K, e));
     RF_TRY_LAUNCH("rf_gemm_kernel");
     return RF_OK;
 }
 
+template <int BN, int CG>
+static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStream_t st) {
+    switch (epi) {
+        case gemm::kStoreBF16: return launch<BN, gemm::kStoreBF16, CG>(p, e, st);
+        case gemm::kStoreF32: return launch<BN, gemm::kStoreF32, CG>(p, e, st);
+        case gemm::kResidGate: return launch<BN, gemm::kResidGate, CG>(p, e, st);
+        case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG>(p, e, st);
+        case gemm::kStoreF32Scale: return launch<BN, gemm::kStoreF32Scale, CG>(p, e, st);
+        case gemm::kBF16Rope: return launch<BN, gemm::kBF16Rope, CG>(p, e, st);
+    }
+    set_error("gemm: bad epilogue %d", epi);
+    return RF_EINVAL;
+}
+
 int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, int64_t K, int64_t lda,
-              int64_t ldb, int bn) {
-    if (K % gemm::BK || (bn != 128 && bn != 256) || N % bn || M < 1) {
-        set_error("gemm: unsupported shape M=%lld N=%lld K=%lld BN=%d", (long long)M, (long long)N,
-                  (long long)K, bn);
+              int64_t ldb, int bn, int cg) {
+    if (K % gemm::BK || (bn != 128 && bn != 256) || (cg != 1 && cg != 2) || N % bn || M < 1) {
+        set_error("gemm: unsupported shape M=%lld N=%lld K=%lld BN=%d CG=%d", (long long)M, (long long)N,
+                  (long long)K, bn, cg);
         return RF_EINVAL;
     }
     p->M = M;
     p->N = N;
     p->K = K;
     p->bn = bn;
+    p->cg = cg;
     int rc = make_tmap_bf16_2d(&p->ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, gemm::BK, gemm::BM);
     if (rc) return rc;
-    return make_tmap_bf16_2d(&p->tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, gemm::BK, (uint32_t)bn);
+    return make_tmap_bf16_2d(&p->tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, gemm::BK, (uint32_t)(bn / cg));
+}
+
+static unsigned long long *g_trace = nullptr;   // debugging timeline buffer (rf_gemm_set_trace)
+
+int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo) {
+    p->c_ptr = out;
+    p->c_ld = ldo;
+    p->c_rows = p->M;   // stores clip at M rows
+    // fp32 [M, N] with row stride ldo, 32 x 32 boxes (128-byte rows: SWIZZLE_128B)
+    return make_tmap_f32_2d(&p->tc, out, (uint64_t)p->N, (uint64_t)p->M, (uint64_t)ldo * 4, 32, 32);
 }
 
 int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,
@@ -83,46 +133,38 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
     // The tensor maps cover the plan's (maximum) M; a smaller M only shortens the tile walk.
     GemmPlan p = plan;
     if (M > 0 && M < p.M) p.M = M;
+    if (epi == gemm::kResidGate && p.bn == 128 && (p.c_ptr != out || p.c_ld != ldo || p.c_rows != p.M)) {
+        // the TMA-staged residual epilogue needs a map over `out` (cached when planned)
+        int rc = gemm_plan_c(&p, out, ldo);
+        if (rc) return rc;
+    }
     gemm::EpiArgs e{out, ldo, gate, gate_ld, rows_per_batch > 0 ? rows_per_batch : 1, alpha, rope, rope_cols,
                     vt ? (__nv_bfloat16 *)vt->ptr : nullptr, vt ? vt->col0 : 0, vt ? vt->heads : 0,
-                    vt ? vt->ld : 0};
-    if (p.bn == 256) {
-        switch (epi) {
-            case gemm::kStoreBF16: return launch<256, gemm::kStoreBF16>(p, e, st);
-            case gemm::kStoreF32: return launch<256, gemm::kStoreF32>(p, e, st);
-            case gemm::kResidGate: return launch<256, gemm::kResidGate>(p, e, st);
-            case gemm::kSwiGLU: return launch<256, gemm::kSwiGLU>(p, e, st);
-            case gemm::kStoreF32Scale: return launch<256, gemm::kStoreF32Scale>(p, e, st);
-            case gemm::kBF16Rope: return launch<256, gemm::kBF16Rope>(p, e, st);
-        }
-    } else {
-        switch (epi) {
-            case gemm::kStoreBF16: return launch<128, gemm::kStoreBF16>(p, e, st);
-            case gemm::kStoreF32: return launch<128, gemm::kStoreF32>(p, e, st);
-            case gemm::kResidGate: return launch<128, gemm::kResidGate>(p, e, st);
-            case gemm::kSwiGLU: return launch<128, gemm::kSwiGLU>(p, e, st);
-            case gemm::kStoreF32Scale: return launch<128, gemm::kStoreF32Scale>(p, e, st);
-            case gemm::kBF16Rope: return launch<128, gemm::kBF16Rope>(p, e, st);
-        }
-    }
-    set_error("gemm: bad epilogue %d", epi);
-    return RF_EINVAL;
+                    vt ? vt->ld : 0, vt ? vt->period : 0, vt ? vt->layer_stride : 0, g_trace};
+    if (p.bn == 256) return p.cg == 2 ? dispatch<256, 2>(p, epi, e, st) : dispatch<256, 1>(p, epi, e, st);
+    return p.cg == 2 ? dispatch<128, 2>(p, epi, e, st) : dispatch<128, 1>(p, epi, e, st);
 }
 
 }  // namespace rf
 
 using namespace rf;
 
+// Debugging aid (not part of the product ABI): when set, every GEMM launch records a
+// clock64 timeline per CTA into buf ([cta][tile < 16][8] u64) -- see tools/gemm_trace.py.
+extern "C" void rf_gemm_set_trace(void *buf) { g_trace = (unsigned long long *)buf; }
+
 extern "C" int rf_gemm_bf16(const void *A, const void *B, void *out, int64_t M, int64_t N, int64_t K,
                             int64_t lda, int64_t ldb, int64_t ldo, int32_t epilogue, const float *gate,
                             int64_t gate_ld, int32_t rows_per_batch, float alpha, int32_t block_n,
                             void *stream) {
+    // block_n: 128 / 256 = one CTA per 128 x block_n tile; -128 / -256 = a CTA pair
+    // (cta_group::2) per 256 x |block_n| tile
     if (!A || !B || !out || (epilogue == gemm::kResidGate && !gate) || epilogue == gemm::kBF16Rope) {
         set_error("rf_gemm_bf16: null argument");
         return RF_EINVAL;
     }
     GemmPlan p;
-    int rc = gemm_plan(&p, A, B, M, N, K, lda, ldb, block_n);
+    int rc = gemm_plan(&p, A, B, M, N, K, lda, ldb, block_n < 0 ? -block_n : block_n, block_n < 0 ? 2 : 1);
     if (rc) return rc;
     return gemm_run(p, epilogue, out, ldo, gate, gate_ld, rows_per_batch, alpha, (cudaStream_t)stream);
 }

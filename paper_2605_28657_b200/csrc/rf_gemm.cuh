@@ -37,73 +37,128 @@ struct EpiArgs {
     // kBF16Rope: columns >= vt_col0 (the V heads) are written transposed instead, to
     // vt[((b * vt_heads + hv) * 128 + dim) * vt_ld + pos] (b = m / rows_per_batch) -- the
     // K-major B operand of the attention's P V^T product.
+    // With vt_period > 0 the columns repeat in groups of vt_period (one group per layer of
+    // a batched all-layer projection): within-group column c = n % vt_period, group
+    // g = n / vt_period, and group g's V^T block starts vt_layer_stride elements later.
     __nv_bfloat16 *vt;
     int vt_col0, vt_heads;
     int64_t vt_ld;
+    int vt_period;
+    int64_t vt_layer_stride;
+    // debugging: per-CTA clock64 timeline ([cta][tile < 16][8]); null in production
+    unsigned long long *trace;
 };
 
+#define RF_TRACE(tile, slot)                                                                          \
+    do {                                                                                              \
+        if (epi.trace && (tile) < 16)                                                                 \
+            epi.trace[((size_t)blockIdx.x * 16 + (tile)) * 8 + (slot)] = (unsigned long long)clock64(); \
+    } while (0)
+
 constexpr int BM = 128, BK = 64;
-template <int BN>
+// CG = 1: one CTA per 128 x BN tile.  CG = 2: a CTA pair ((2,1,1) cluster) per 256 x BN
+// tile -- each CTA stages its own 128 A rows and BN/2 of the B rows, the even CTA issues
+// tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' shared memory, and each CTA's
+// TMEM receives its own 128 accumulator rows.  Per-SM shared-memory operand traffic per
+// FLOP drops by a third (BN = 256) to a quarter (BN = 128).
+// TMA_C (the gated-residual epilogue at BN = 128): each epilogue warp prefetches its 32 x BN
+// fp32 slice of the residual stream into shared memory with TMA (issued before the
+// accumulator is ready, so the read overlaps the main loop), updates it in place from TMEM,
+// and writes it back with a TMA store -- instead of row-per-thread global loads/stores.
+template <int BN, int CG = 1, int EPI = 0>
 struct Cfg {
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int BN_LOAD = BN / CG;   // B rows staged by each CTA
     static constexpr uint32_t A_BYTES = BM * BK * 2;
-    static constexpr uint32_t B_BYTES = BN * BK * 2;
-    static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+    static constexpr uint32_t B_BYTES = BN_LOAD * BK * 2;
+    static constexpr bool TMA_C = EPI == 2 && BN == 128;
+    static constexpr int C_COLS = 64;                                           // staged per pass
+    static constexpr uint32_t C_WARP_BYTES = TMA_C ? 32u * C_COLS * 4u : 0u;   // per epilogue warp
+    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES;
+    // as many operand stages as fit next to the epilogue staging (227 KB opt-in limit)
+    static constexpr uint32_t BUDGET = 232448u - 1024u - 512u - C_BYTES;
+    static constexpr int STAGES = (int)(BUDGET / (A_BYTES + B_BYTES)) > 10 ? 10 : (int)(BUDGET / (A_BYTES + B_BYTES));
+    static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + 512;
 };
 
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG = 1>
 __global__ void __launch_bounds__(192, 1)
-rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, int M,
-               int N, int K, EpiArgs epi) {
+rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+               const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, EpiArgs epi) {
     using namespace rf::sm100;
-    using C = Cfg<BN>;
+    using C = Cfg<BN, CG, EPI>;
+    constexpr int TM = BM * CG;   // output rows per tile (per CTA pair when CG = 2)
     constexpr int STAGES = C::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = base;
     uint8_t *sB = base + STAGES * C::A_BYTES;
-    uint64_t *full = (uint64_t *)(sB + STAGES * C::B_BYTES);
+    uint8_t *sC = sB + STAGES * C::B_BYTES;   // C_BYTES (1024-aligned: stage sizes are multiples of 1 KB)
+    uint64_t *full = (uint64_t *)(sC + C::C_BYTES);
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+    uint64_t *cfull = tempty + 2;            // [4] one per epilogue warp (TMA_C)
+    uint32_t *tmem_slot = (uint32_t *)(cfull + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;   // 0 = leader (issues the MMAs)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
+        if constexpr (C::TMA_C) tma_prefetch(&tma_c);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 4 * CG);   // the epilogue warps of both CTAs release the leader
         }
+        for (int i = 0; i < 4; ++i) mbar_init(&cfull[i], 1);
         mbar_fence_init();
     }
-    if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (CG == 2)
+            tmem_alloc_pair<2 * BN>(tmem_slot);
+        else
+            tmem_alloc<2 * BN>(tmem_slot);
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2)
+        cluster_sync();   // peer barriers initialised before any remote arrive / complete_tx
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const int num_m = (M + BM - 1) / BM, num_n = N / BN, kblocks = K / BK;
+    const int num_m = (M + TM - 1) / TM, num_n = N / BN, kblocks = K / BK;
     const int num_tiles = num_m * num_n;
+    const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile walker id
+    const int units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
     if (warp == 0) {
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-                const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+            int it = 0;
+            for (int t = unit; t < num_tiles; t += units, ++it) {
+                const int m0 = (t % num_m) * TM + (int)rank * BM, n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
+                RF_TRACE(it, 6);
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
-                    tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * BK, m0);
-                    tma_load_2d(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0);
+                    if constexpr (CG == 2) {
+                        // both CTAs' bytes complete on the leader's full barrier
+                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+                        const uint32_t fb = mapa_shared(&full[stage], 0);
+                        tma_load_2d_pair(sA + stage * C::A_BYTES, &tma_a, fb, kb * BK, m0);
+                        tma_load_2d_pair(sB + stage * C::B_BYTES, &tma_b, fb, kb * BK, n0);
+                    } else {
+                        mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+                        tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * BK, m0);
+                        tma_load_2d(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -112,44 +167,133 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             }
         }
     } else if (warp == 1) {
-        if (elect_one()) {
-            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+        if (rank == 0 && elect_one()) {
+            constexpr uint32_t idesc = idesc_bf16(TM, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            int it = 0;
+            for (int t = unit; t < num_tiles; t += units, ++it) {
+                RF_TRACE(it, 0);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
+                RF_TRACE(it, 1);
                 const uint32_t d_tmem = tmem + acc * BN;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    if (kb == 0) RF_TRACE(it, 2);
                     const uint64_t ad = sdesc_sw128(sA + stage * C::A_BYTES);
                     const uint64_t bd = sdesc_sw128(sB + stage * C::B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
-                                  (kb | k) != 0);
-                    umma_commit(&empty[stage]);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        if constexpr (CG == 2)
+                            umma_bf16_pair(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                                           (kb | k) != 0);
+                        else
+                            umma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                                      (kb | k) != 0);
+                    }
+                    if constexpr (CG == 2)
+                        umma_commit_pair(&empty[stage]);
+                    else
+                        umma_commit(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                RF_TRACE(it, 3);
+                if constexpr (CG == 2)
+                    umma_commit_pair(&tfull[acc]);
+                else
+                    umma_commit(&tfull[acc]);
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
             }
         }
+    } else if constexpr (C::TMA_C) {
+        // gated residual, TMA-staged: out[m, n] += gate[m / rows_per_batch, n] * acc
+        const int q = warp & 3;
+        uint8_t *sw = sC + q * C::C_WARP_BYTES;   // C_COLS/32 boxes of [32 rows][32 fp32], SWIZZLE_128B
+        constexpr int NB = C::C_COLS / 32;
+        int acc = 0, it = 0;
+        uint32_t acc_phase = 0, c_phase = 0;
+        for (int t = unit; t < num_tiles; t += units, ++it) {
+            const int m0 = (t % num_m) * TM + (int)rank * BM + q * 32, n0 = (t / num_m) * BN;
+            const int m = m0 + lane;
+            const float *g = epi.gate + (int64_t)(min(m, M - 1) / epi.rows_per_batch) * epi.gate_ld + n0;
+            if (lane == 0)   // later passes' residual slices -> L2 now, so their loads below are L2 hits
+                for (int j = NB; j < BN / 32; ++j) tma_prefetch_l2_2d(&tma_c, n0 + j * 32, m0);
+#pragma unroll 1
+            for (int p0 = 0; p0 < BN; p0 += C::C_COLS) {
+                if (lane == 0) {
+                    // the pass's residual slice; the first one is in flight while the MMAs run
+                    bulk_wait_read0();   // the previous store has finished reading sw
+                    mbar_expect_tx(&cfull[q], C::C_WARP_BYTES);
+#pragma unroll
+                    for (int j = 0; j < NB; ++j)
+                        tma_load_2d(sw + j * 4096, &tma_c, &cfull[q], n0 + p0 + j * 32, m0);
+                }
+                if (p0 == 0) {
+                    mbar_wait(&tfull[acc], acc_phase);
+                    tc_fence_after();
+                    if (q == 2 && lane == 0) RF_TRACE(it, 4);
+                }
+                mbar_wait(&cfull[q], c_phase);
+                c_phase ^= 1;
+#pragma unroll 1
+                for (int j = 0; j < NB; ++j) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + p0 + j * 32), r);
+                    float4 gv[8];
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) gv[v] = __ldg((const float4 *)(g + p0 + j * 32 + v * 4));
+                    tmem_ld_wait();
+                    float4 *row = (float4 *)(sw + j * 4096 + lane * 128);
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        float4 x = row[v ^ (lane & 7)];
+                        x.x += gv[v].x * __uint_as_float(r[4 * v]);
+                        x.y += gv[v].y * __uint_as_float(r[4 * v + 1]);
+                        x.z += gv[v].z * __uint_as_float(r[4 * v + 2]);
+                        x.w += gv[v].w * __uint_as_float(r[4 * v + 3]);
+                        row[v ^ (lane & 7)] = x;
+                    }
+                }
+                fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) tma_store_2d(&tma_c, sw + j * 4096, n0 + p0 + j * 32, m0);
+                    bulk_commit();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (q == 2) RF_TRACE(it, 5);
+                if constexpr (CG == 2)
+                    mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+                else
+                    mbar_arrive(&tempty[acc]);
+            }
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (lane == 0) bulk_wait0();
     } else {
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        int acc = 0;
+        int acc = 0, it = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-            const int m0 = (t % num_m) * BM, n0 = (t / num_m) * BN;
+        for (int t = unit; t < num_tiles; t += units, ++it) {
+            const int m0 = (t % num_m) * TM + (int)rank * BM, n0 = (t / num_m) * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (q == 2 && lane == 0) RF_TRACE(it, 4);
             const int m = m0 + q * 32 + lane;
             const bool live = m < M;
 #pragma unroll 1
@@ -174,10 +318,13 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         *(uint4 *)(o + v * 8) = pk;
                     }
                 } else if constexpr (EPI == kBF16Rope) {
-                    if (epi.vt && n >= epi.vt_col0) {
-                        const int cv = n - epi.vt_col0, hv = cv >> 7, dim0 = cv & 127;
+                    const int nl = epi.vt_period ? n % epi.vt_period : n;
+                    if (epi.vt && nl >= epi.vt_col0) {
+                        const int cv = nl - epi.vt_col0, hv = cv >> 7, dim0 = cv & 127;
                         const int64_t b = m / epi.rows_per_batch, pos = m % epi.rows_per_batch;
-                        __nv_bfloat16 *dst = epi.vt + ((b * epi.vt_heads + hv) * 128 + dim0) * epi.vt_ld + pos;
+                        const int64_t grp = epi.vt_period ? n / epi.vt_period : 0;
+                        __nv_bfloat16 *dst = epi.vt + grp * epi.vt_layer_stride +
+                                             ((b * epi.vt_heads + hv) * 128 + dim0) * epi.vt_ld + pos;
 #pragma unroll
                         for (int e = 0; e < 32; ++e)   // lanes hold consecutive tokens: coalesced
                             dst[(int64_t)e * epi.vt_ld] = __float2bfloat16(__uint_as_float(r[e]));
@@ -258,15 +405,27 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (q == 2) RF_TRACE(it, 5);
+                if constexpr (CG == 2)
+                    mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+                else
+                    mbar_arrive(&tempty[acc]);
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
         }
     }
-    __syncthreads();
-    if (warp == 1) tmem_dealloc<2 * BN>(tmem);
+    if constexpr (CG == 2) {
+        tc_fence_before();
+        cluster_sync();   // the leader's MMAs and commits into this CTA are done
+        if (warp == 1) tmem_dealloc_pair<2 * BN>(tmem);
+    } else {
+        __syncthreads();
+        if (warp == 1) tmem_dealloc<2 * BN>(tmem);
+    }
 }
 
 }  // namespace rf::gemm

@@ -8,19 +8,29 @@ namespace rf {
 
 struct GemmPlan {
     CUtensorMap ta, tb;
+    CUtensorMap tc;             // fp32 output map of the TMA-staged residual epilogue
+    void *c_ptr = nullptr;
+    int64_t c_ld = 0, c_rows = 0;
     int64_t M, N, K;
     int bn;
+    int cg;   // 1: 128 x bn tiles per CTA; 2: 256 x bn tiles per CTA pair (cta_group::2)
 };
 
 int make_tmap_bf16_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                       uint32_t box_inner, uint32_t box_outer);
+int make_tmap_f32_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                     uint32_t box_inner, uint32_t box_outer);
+// bind the residual-stream output of a kResidGate plan (builds its TMA map once)
+int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo);
 int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, int64_t K, int64_t lda,
-              int64_t ldb, int bn);
+              int64_t ldb, int bn, int cg = 1);
 // Transposed V output of the QKV / cross-KV GEMM (see EpiArgs::vt).
 struct VtOut {
     void *ptr;
     int col0, heads;
     int64_t ld;
+    int period = 0;             // > 0: column groups of this width, one V^T block per group
+    int64_t layer_stride = 0;   // elements between the groups' V^T blocks
 };
 
 int gemm_run(const GemmPlan &p, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,

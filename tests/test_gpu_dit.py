@@ -46,16 +46,22 @@ def test_attention_vs_sdpa(dit_mod, B, Nq, Nk, H, Hk):
     assert rel_rms(out, ref) < 1e-2
 
 
-@pytest.mark.parametrize("B,Nq,Nk,H,Hk", [(2, 750, 750, 16, 8), (1, 100, 37, 4, 4), (3, 750, 128, 16, 8),
-                                          (1, 128, 128, 2, 1), (2, 300, 1000, 4, 2)])
-def test_tcgen05_attention_vs_sdpa(dit_mod, B, Nq, Nk, H, Hk):
+@pytest.mark.parametrize("B,Nq,Nk,H,Hk,grow", [(2, 750, 750, 16, 8, 0), (1, 100, 37, 4, 4, 0), (3, 750, 128, 16, 8, 0),
+                                               (1, 128, 128, 2, 1, 0), (2, 300, 1000, 4, 2, 0),
+                                               (2, 256, 900, 4, 2, 1), (1, 200, 640, 2, 2, 1)])
+def test_tcgen05_attention_vs_sdpa(dit_mod, B, Nq, Nk, H, Hk, grow):
+    """grow: key norms rise along the sequence, so the running row max climbs tile after
+    tile (exercises the lazy O/l rescaling of the single-pass kernel)."""
     from paper_2605_28657_b200 import _native
 
     lib = _native.load()
     lib.rf_attention_tc_bf16.restype = int
     g = torch.Generator(device="cuda").manual_seed(Nq * 11 + Nk)
     q = torch.randn(B * Nq, H * 128, device="cuda", generator=g).bfloat16()
-    k = torch.randn(B * Nk, Hk * 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B * Nk, Hk * 128, device="cuda", generator=g)
+    if grow:
+        k = k * torch.linspace(0.3, 4.0, Nk, device="cuda").repeat(B)[:, None]
+    k = k.bfloat16()
     v = torch.randn(B * Nk, Hk * 128, device="cuda", generator=g).bfloat16()
     nk_pad = (Nk + 7) // 8 * 8
     vt = torch.zeros(B, Hk, 128, nk_pad, device="cuda", dtype=torch.bfloat16)

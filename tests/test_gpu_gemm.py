@@ -16,14 +16,16 @@ def ref(a, b):
     return a.float() @ b.float().T
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("M,N,K,bn", [(128, 128, 64, 128), (200, 256, 128, 256), (3000, 2048, 2048, 256),
                                       (3000, 2048, 2048, 128), (1, 256, 64, 256), (517, 384, 640, 128),
-                                      (3000, 12288, 2048, 256)])
-def test_gemm_f32_matches_torch(ops, M, N, K, bn):
+                                      (3000, 12288, 2048, 256), (3000, 4096, 2048, 256), (3000, 2048, 6144, 128),
+                                      (129, 256, 64, 128)])
+def test_gemm_f32_matches_torch(ops, M, N, K, bn, pair):
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     b = torch.randn(N, K, device="cuda", generator=g).bfloat16()
-    out = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=bn)
+    out = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=bn, pair=pair)
     r = ref(a, b)
     err = (out - r).abs().max().item() / r.abs().max().item()
     assert err < 1e-5, err
@@ -39,25 +41,27 @@ def test_gemm_bf16_and_scale(ops):
     assert torch.allclose(s, 0.25 * r, rtol=1e-5, atol=1e-3)
 
 
-def test_gemm_resid_gate(ops):
-    B, T, K, N = 3, 100, 256, 512
+@pytest.mark.parametrize("pair", [False, True])
+@pytest.mark.parametrize("B,T,K,N", [(3, 100, 256, 512), (4, 750, 2048, 2048), (1, 77, 128, 256)])
+def test_gemm_resid_gate(ops, pair, B, T, K, N):
     a = torch.randn(B * T, K, device="cuda").bfloat16()
     b = torch.randn(N, K, device="cuda").bfloat16()
     gate = torch.randn(B, N, device="cuda")
     x0 = torch.randn(B * T, N, device="cuda")
     x = x0.clone()
-    ops.gemm(a, b, out=x, epilogue=ops.EPI_RESID_GATE, gate=gate, rows_per_batch=T)
+    ops.gemm(a, b, out=x, epilogue=ops.EPI_RESID_GATE, gate=gate, rows_per_batch=T, block_n=128, pair=pair)
     r = x0 + gate.repeat_interleave(T, 0) * ref(a, b)
     assert torch.allclose(x, r, rtol=1e-5, atol=1e-3)
 
 
-def test_gemm_swiglu(ops):
+@pytest.mark.parametrize("pair", [False, True])
+def test_gemm_swiglu(ops, pair):
     M, K, H = 260, 256, 384
     a = torch.randn(M, K, device="cuda").bfloat16()
     wg = torch.randn(H, K, device="cuda").bfloat16() * 0.1
     wu = torch.randn(H, K, device="cuda").bfloat16() * 0.1
     w = torch.stack([wg, wu], 1).reshape(2 * H, K).contiguous()   # interleaved (g, u) rows
-    out = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256)
+    out = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256, pair=pair)
     g, u = ref(a, wg).bfloat16().float(), ref(a, wu).bfloat16().float()
     r = torch.nn.functional.silu(g) * u
     assert torch.allclose(out.float(), r, rtol=2e-2, atol=2e-2)

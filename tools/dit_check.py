@@ -34,6 +34,25 @@ def main():
     ms = a.elapsed_time(b) / n
     fl = cfg.flops_per_forward(rows, 1500)
     print(f"forward {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s  ({fl / 1e12:.2f} TFLOP)  params={cfg.params() / 1e9:.2f}B")
+    if "--graph" in sys.argv:   # same forward replayed from a CUDA graph (no host launch gaps)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            dit.forward(xs, ts, conds)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                dit.forward(xs, ts, conds)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(n):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        gms = a.elapsed_time(b) / n
+        print(f"graph forward {gms:.3f} ms  {fl / gms / 1e9:.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
