@@ -81,27 +81,50 @@ rf_dit_norm_mod(const float *__restrict__ h, int64_t rows, int tokens, const flo
     }
 }
 
+// Per-call row inputs.  They live in device memory (written by rf_dit_set_rows at the start
+// of every forward) so the rest of the forward is a fixed launch sequence that is captured
+// once per row count into a CUDA graph and replayed.
 struct RowPtrs {
     const double *x[kMaxDitRows];
+    const __nv_bfloat16 *cond[kMaxDitRows];
     float t[kMaxDitRows];
 };
 
+__global__ void rf_dit_set_rows(const __grid_constant__ RowPtrs R, RowPtrs *dst) {
+    const int i = threadIdx.x;
+    if (i < kMaxDitRows) {
+        dst->x[i] = R.x[i];
+        dst->cond[i] = R.cond[i];
+        dst->t[i] = R.t[i];
+    }
+}
+
 // x (float64 ring rows, [T*C] each) -> bf16 patch tokens [B, N, p*C] (a flat per-row cast).
-__global__ void rf_dit_patchify(const __grid_constant__ RowPtrs R, int64_t per_row, __nv_bfloat16 *out) {
+__global__ void rf_dit_patchify(const RowPtrs *__restrict__ R, int64_t per_row, __nv_bfloat16 *out) {
     const int b = blockIdx.y;
+    const double *x = R->x[b];
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i < per_row;
          i += (int64_t)gridDim.x * blockDim.x * 2) {
-        const double2 v = *(const double2 *)(R.x[b] + i);
+        const double2 v = *(const double2 *)(x + i);
         *(__nv_bfloat162 *)(out + b * per_row + i) = __floats2bfloat162_rn((float)v.x, (float)v.y);
     }
 }
 
+// the rows' conditioning tokens, gathered into one [B * n_cond, D] operand (16-byte copies)
+__global__ void rf_dit_gather_cond(const RowPtrs *__restrict__ R, int64_t per_row, __nv_bfloat16 *out) {
+    const int b = blockIdx.y;
+    const uint4 *src = (const uint4 *)R->cond[b];
+    uint4 *dst = (uint4 *)(out + b * per_row);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_row / 8; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 // sinusoidal timestep features [cos | sin] of 1000 * t (bf16 [Bpad, F]).
-__global__ void rf_dit_tfeat(const __grid_constant__ RowPtrs R, int B, int F, __nv_bfloat16 *out) {
+__global__ void rf_dit_tfeat(const RowPtrs *__restrict__ R, int B, int F, __nv_bfloat16 *out) {
     const int b = blockIdx.x, half = F / 2;
     for (int i = threadIdx.x; i < half; i += blockDim.x) {
         const float freq = expf(-logf(10000.f) * (float)i / (float)half);
-        const float arg = 1000.f * R.t[b] * freq;
+        const float arg = 1000.f * R->t[b] * freq;
         float s, c;
         sincosf(arg, &s, &c);
         out[(int64_t)b * F + i] = __float2bfloat16(c);
@@ -144,6 +167,11 @@ struct Dit {
     int64_t vt_cross_layer;                // elements per layer block of vt_cross
     AttnPlan a_self;
     std::vector<AttnPlan> a_cross;
+    RowPtrs *rows_dev;                       // per-call row inputs (rf_dit_set_rows)
+    // one CUDA graph of the forward body per row count (and output buffer)
+    cudaGraphExec_t graph[kMaxDitRows + 1] = {};
+    float *graph_out[kMaxDitRows + 1] = {};
+    bool use_graphs;
     bool tc_attention;
     // GEMM plans (tensor maps at max rows)
     GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out, p_kvc;
@@ -178,6 +206,7 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
     const int64_t n_pad = (N + 7) / 8 * 8, nc_pad = (c.n_cond_tokens + 7) / 8 * 8;
     void *vt_self = take((int64_t)max_rows * kv_dim * n_pad * 2);
     void *vt_cross = take((int64_t)c.n_layers * max_rows * kv_dim * nc_pad * 2);
+    void *rows_dev = take(sizeof(RowPtrs));
     if (d) {
         d->xin = (__nv_bfloat16 *)xin;
         d->a = (__nv_bfloat16 *)a;
@@ -198,6 +227,7 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
         d->rope = (float2 *)rope;
         d->vt_self = (__nv_bfloat16 *)vt_self;
         d->vt_cross = (__nv_bfloat16 *)vt_cross;
+        d->rows_dev = (RowPtrs *)rows_dev;
         d->n_pad = (int)n_pad;
         d->nc_pad = (int)nc_pad;
         d->vt_cross_layer = (int64_t)max_rows * kv_dim * nc_pad;
@@ -311,6 +341,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         return rc;
     }
     d->tc_attention = getenv("RF_ATTN_MMA_SYNC") == nullptr;   // the tcgen05 kernel is the default
+    d->use_graphs = getenv("RF_DIT_NO_GRAPH") == nullptr;
     // V^T pad columns are never written: zero them once
     RF_TRY_CUDA(cudaMemsetAsync(d->vt_self, 0, (size_t)max_rows * d->kv_dim * d->n_pad * 2, (cudaStream_t)stream));
     RF_TRY_CUDA(cudaMemsetAsync(d->vt_cross, 0, (size_t)L * d->vt_cross_layer * 2, (cudaStream_t)stream));
@@ -321,7 +352,11 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
 }
 
 extern "C" int rf_dit_destroy(void *handle) {
-    delete (Dit *)handle;
+    Dit *d = (Dit *)handle;
+    if (d)
+        for (auto &g : d->graph)
+            if (g) cudaGraphExecDestroy(g);
+    delete d;
     return RF_OK;
 }
 
@@ -344,27 +379,16 @@ static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shi
         if (_r) return _r;     \
     } while (0)
 
-extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x_rows, const float *t_rows,
-                              const void *const *cond_rows, float *v_out, void *stream) {
-    Dit *dp = (Dit *)handle;
-    if (!dp || rows < 1 || rows > dp->max_rows || !x_rows || !t_rows || !cond_rows) {
-        set_error("rf_dit_forward: bad arguments (rows=%d)", rows);
-        return RF_EINVAL;
-    }
-    const Dit &d = *dp;
+// The forward body: a fixed launch sequence for a given row count and output buffer
+// (every per-call input is read from d.rows_dev), so it can be captured into a graph.
+static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
     const rf_dit_config &c = d.c;
-    cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = d.tokens, M = (int64_t)rows * N, D = c.d_model, L = c.n_layers, B = rows;
     const int64_t W6 = 6 * D, Nc = c.n_cond_tokens;
-    RowPtrs R{};
-    for (int b = 0; b < rows; ++b) {
-        R.x[b] = x_rows[b];
-        R.t[b] = t_rows[b];
-    }
     // patch tokens and timestep conditioning
-    rf_dit_patchify<<<dim3(64, rows), 256, 0, st>>>(R, (int64_t)d.frames * c.latent_channels, d.xin);
+    rf_dit_patchify<<<dim3(64, rows), 256, 0, st>>>(d.rows_dev, (int64_t)d.frames * c.latent_channels, d.xin);
     RF_TRY_LAUNCH("rf_dit_patchify");
-    rf_dit_tfeat<<<rows, 128, 0, st>>>(R, rows, c.freq_dim, d.tfeat);
+    rf_dit_tfeat<<<rows, 128, 0, st>>>(d.rows_dev, rows, c.freq_dim, d.tfeat);
     RF_TRY_LAUNCH("rf_dit_tfeat");
     RF_TRY(gemm_run(d.p_t1, RF_EPI_F32, d.tmp, D, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
     rf_dit_silu_bf16<<<64, 256, 0, st>>>(d.tmp, d.tbuf, B * D);
@@ -375,9 +399,8 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
     rf_dit_layer_mods<<<256, 256, 0, st>>>(d.w.ada_table, d.mod, d.mods, (int)L, (int)B, (int)W6);
     RF_TRY_LAUNCH("rf_dit_layer_mods");
     // conditioning tokens of every row
-    for (int b = 0; b < rows; ++b)
-        RF_TRY_CUDA(cudaMemcpyAsync(d.cond + (int64_t)b * Nc * D, cond_rows[b], Nc * D * 2,
-                                    cudaMemcpyDeviceToDevice, st));
+    rf_dit_gather_cond<<<dim3(64, rows), 256, 0, st>>>(d.rows_dev, Nc * D, d.cond);
+    RF_TRY_LAUNCH("rf_dit_gather_cond");
     // cross-attention K (and V^T for the tcgen05 attention) of every layer, one GEMM
     {
         const VtOut vtc{d.vt_cross, (int)d.kv_dim, c.n_kv_heads, d.nc_pad, (int)(2 * d.kv_dim), d.vt_cross_layer};
@@ -417,6 +440,52 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
     // final AdaLN + output projection (fp32), tokens [B, N, p*C] == latent [B, T, C]
     RF_TRY(norm_mod(d, d.h, M, d.fmod, d.fmod + D, 2 * D, d.a, st));
     RF_TRY(gemm_run(d.p_out, RF_EPI_F32, v_out ? v_out : d.vout, d.in_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+    return RF_OK;
+}
+
+extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x_rows, const float *t_rows,
+                              const void *const *cond_rows, float *v_out, void *stream) {
+    Dit *dp = (Dit *)handle;
+    if (!dp || rows < 1 || rows > dp->max_rows || !x_rows || !t_rows || !cond_rows) {
+        set_error("rf_dit_forward: bad arguments (rows=%d)", rows);
+        return RF_EINVAL;
+    }
+    Dit &d = *dp;
+    cudaStream_t st = (cudaStream_t)stream;
+    RowPtrs R{};
+    for (int b = 0; b < rows; ++b) {
+        R.x[b] = x_rows[b];
+        R.t[b] = t_rows[b];
+        R.cond[b] = (const __nv_bfloat16 *)cond_rows[b];
+    }
+    rf_dit_set_rows<<<1, kMaxDitRows, 0, st>>>(R, d.rows_dev);
+    RF_TRY_LAUNCH("rf_dit_set_rows");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    RF_TRY_CUDA(cudaStreamIsCapturing(st, &cap));
+    // graphs need a capturable stream (not the legacy default stream) and no outer capture
+    if (!d.use_graphs || st == 0 || cap != cudaStreamCaptureStatusNone) return dit_body(d, rows, v_out, st);
+    if (!d.graph[rows] || d.graph_out[rows] != v_out) {
+        if (d.graph[rows]) {
+            cudaGraphExecDestroy(d.graph[rows]);
+            d.graph[rows] = nullptr;
+        }
+        RF_TRY(dit_body(d, rows, v_out, st));   // first call: direct (one-time kernel attributes)
+        cudaGraph_t g = nullptr;
+        RF_TRY_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const int rc = dit_body(d, rows, v_out, st);
+        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        RF_TRY_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&d.graph[rows], g, 0);
+        cudaGraphDestroy(g);
+        RF_TRY_CUDA(ie);
+        d.graph_out[rows] = v_out;
+        return RF_OK;
+    }
+    RF_TRY_CUDA(cudaGraphLaunch(d.graph[rows], st));
     return RF_OK;
 }
 
