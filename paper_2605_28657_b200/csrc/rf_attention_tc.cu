@@ -344,6 +344,8 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_launch();
 
     if (warp == TMA_WARP) {
         if (elect_one()) {
@@ -544,8 +546,8 @@ static int launch_fa(const AttnPlan &p, void *out, int64_t ldo, int B, float sc,
         attr = true;
     }
     dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / NH);
-    rf_attn_fa_kernel<NH><<<grid, 128 * NH + 64, fa_smem<NH>(), st>>>(p.tq, p.tk, p.tvt, (__nv_bfloat16 *)out, ldo,
-                                                                     p.Nq, p.Nk, p.H, p.Hkv, sc);
+    RF_TRY_CUDA(launch_pdl(rf_attn_fa_kernel<NH>, grid, dim3(128 * NH + 64), fa_smem<NH>(), st, p.tq, p.tk, p.tvt,
+                           (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
     RF_TRY_LAUNCH("rf_attn_fa_kernel");
     return RF_OK;
 }

@@ -23,6 +23,31 @@ int check_cuda(cudaError_t e, const char *what);
 
 int sm_count();
 
+// ------------------------------------------------- programmatic dependent launch ----
+// Kernels of the DiT forward are launched with programmatic stream serialization: a
+// kernel's CTAs may start (barrier init, TMEM alloc, descriptor prefetch) while the
+// previous kernel drains, and block in pdl_wait() until its results are visible.  Every
+// such kernel calls pdl_wait() before its first global-memory access and pdl_launch()
+// right after, so at most two grids are in flight.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<Args &&>(args)...);
+}
+
 // ------------------------------------------------------------------ philox --------
 // Philox4x64-10 exactly as numpy's bit generator (numpy/random/src/philox/philox.h).
 struct u64x4 {

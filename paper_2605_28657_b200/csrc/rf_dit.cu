@@ -40,6 +40,8 @@ template <int D>
 __global__ void __launch_bounds__(256)
 rf_dit_norm_mod(const float *__restrict__ h, int64_t rows, int tokens, const float *__restrict__ shift,
                 const float *__restrict__ scale, int64_t mod_ld, __nv_bfloat16 *__restrict__ out, float eps) {
+    pdl_wait();
+    pdl_launch();
     constexpr int PER = D / 32 / 4;  // float4 per lane
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -101,6 +103,8 @@ __global__ void rf_dit_set_rows(const __grid_constant__ RowPtrs R, RowPtrs *dst)
 
 // x (float64 ring rows, [T*C] each) -> bf16 patch tokens [B, N, p*C] (a flat per-row cast).
 __global__ void rf_dit_patchify(const RowPtrs *__restrict__ R, int64_t per_row, __nv_bfloat16 *out) {
+    pdl_wait();
+    pdl_launch();
     const int b = blockIdx.y;
     const double *x = R->x[b];
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; i < per_row;
@@ -112,6 +116,8 @@ __global__ void rf_dit_patchify(const RowPtrs *__restrict__ R, int64_t per_row, 
 
 // the rows' conditioning tokens, gathered into one [B * n_cond, D] operand (16-byte copies)
 __global__ void rf_dit_gather_cond(const RowPtrs *__restrict__ R, int64_t per_row, __nv_bfloat16 *out) {
+    pdl_wait();
+    pdl_launch();
     const int b = blockIdx.y;
     const uint4 *src = (const uint4 *)R->cond[b];
     uint4 *dst = (uint4 *)(out + b * per_row);
@@ -121,6 +127,8 @@ __global__ void rf_dit_gather_cond(const RowPtrs *__restrict__ R, int64_t per_ro
 
 // sinusoidal timestep features [cos | sin] of 1000 * t (bf16 [Bpad, F]).
 __global__ void rf_dit_tfeat(const RowPtrs *__restrict__ R, int B, int F, __nv_bfloat16 *out) {
+    pdl_wait();
+    pdl_launch();
     const int b = blockIdx.x, half = F / 2;
     for (int i = threadIdx.x; i < half; i += blockDim.x) {
         const float freq = expf(-logf(10000.f) * (float)i / (float)half);
@@ -134,6 +142,8 @@ __global__ void rf_dit_tfeat(const RowPtrs *__restrict__ R, int B, int F, __nv_b
 
 // out_bf16 = bf16(silu(in_f32))
 __global__ void rf_dit_silu_bf16(const float *in, __nv_bfloat16 *out, int64_t n) {
+    pdl_wait();
+    pdl_launch();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float x = in[i];
         out[i] = __float2bfloat16(x / (1.f + __expf(-x)));
@@ -142,6 +152,8 @@ __global__ void rf_dit_silu_bf16(const float *in, __nv_bfloat16 *out, int64_t n)
 
 // mods[l][b][j] = table[l][j] + mod[b][j]   (j < 6d)
 __global__ void rf_dit_layer_mods(const float *table, const float *mod, float *mods, int L, int B, int W) {
+    pdl_wait();
+    pdl_launch();
     const int64_t n = (int64_t)L * B * W;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int j = (int)(i % W);
@@ -364,10 +376,10 @@ static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shi
                     int64_t mod_ld, __nv_bfloat16 *out, cudaStream_t st) {
     const unsigned blocks = (unsigned)((rows + 7) / 8);
     switch (d.c.d_model) {
-        case 2048: rf_dit_norm_mod<2048><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
-        case 1024: rf_dit_norm_mod<1024><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
-        case 512: rf_dit_norm_mod<512><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
-        default: rf_dit_norm_mod<256><<<blocks, 256, 0, st>>>(h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps); break;
+        case 2048: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<2048>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
+        case 1024: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<1024>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
+        case 512: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<512>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
+        default: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<256>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
     }
     RF_TRY_LAUNCH("rf_dit_norm_mod");
     return RF_OK;
@@ -386,20 +398,22 @@ static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
     const int64_t N = d.tokens, M = (int64_t)rows * N, D = c.d_model, L = c.n_layers, B = rows;
     const int64_t W6 = 6 * D, Nc = c.n_cond_tokens;
     // patch tokens and timestep conditioning
-    rf_dit_patchify<<<dim3(64, rows), 256, 0, st>>>(d.rows_dev, (int64_t)d.frames * c.latent_channels, d.xin);
+    RF_TRY_CUDA(launch_pdl(rf_dit_patchify, dim3(64, rows), dim3(256), 0, st, (const RowPtrs *)d.rows_dev,
+                           (int64_t)d.frames * c.latent_channels, d.xin));
     RF_TRY_LAUNCH("rf_dit_patchify");
-    rf_dit_tfeat<<<rows, 128, 0, st>>>(d.rows_dev, rows, c.freq_dim, d.tfeat);
+    RF_TRY_CUDA(launch_pdl(rf_dit_tfeat, dim3(rows), dim3(128), 0, st, (const RowPtrs *)d.rows_dev, (int)rows, c.freq_dim, d.tfeat));
     RF_TRY_LAUNCH("rf_dit_tfeat");
     RF_TRY(gemm_run(d.p_t1, RF_EPI_F32, d.tmp, D, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
-    rf_dit_silu_bf16<<<64, 256, 0, st>>>(d.tmp, d.tbuf, B * D);
+    RF_TRY_CUDA(launch_pdl(rf_dit_silu_bf16, dim3(64), dim3(256), 0, st, (const float *)d.tmp, d.tbuf, B * D));
     RF_TRY(gemm_run(d.p_t2, RF_EPI_F32, d.tmp, D, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
-    rf_dit_silu_bf16<<<64, 256, 0, st>>>(d.tmp, d.tbuf, B * D);   // silu(temb)
+    RF_TRY_CUDA(launch_pdl(rf_dit_silu_bf16, dim3(64), dim3(256), 0, st, (const float *)d.tmp, d.tbuf, B * D));   // silu(temb)
     RF_TRY(gemm_run(d.p_ada, RF_EPI_F32, d.mod, W6, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
     RF_TRY(gemm_run(d.p_fada, RF_EPI_F32, d.fmod, 2 * D, nullptr, 0, 1, 1.f, st, nullptr, 0, B));
-    rf_dit_layer_mods<<<256, 256, 0, st>>>(d.w.ada_table, d.mod, d.mods, (int)L, (int)B, (int)W6);
+    RF_TRY_CUDA(launch_pdl(rf_dit_layer_mods, dim3(256), dim3(256), 0, st, (const float *)d.w.ada_table, (const float *)d.mod,
+                           d.mods, (int)L, (int)B, (int)W6));
     RF_TRY_LAUNCH("rf_dit_layer_mods");
     // conditioning tokens of every row
-    rf_dit_gather_cond<<<dim3(64, rows), 256, 0, st>>>(d.rows_dev, Nc * D, d.cond);
+    RF_TRY_CUDA(launch_pdl(rf_dit_gather_cond, dim3(64, rows), dim3(256), 0, st, (const RowPtrs *)d.rows_dev, Nc * D, d.cond));
     RF_TRY_LAUNCH("rf_dit_gather_cond");
     // cross-attention K (and V^T for the tcgen05 attention) of every layer, one GEMM
     {

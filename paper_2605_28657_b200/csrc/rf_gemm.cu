@@ -74,13 +74,15 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
     cfg.blockDim = dim3(192);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CG;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait()
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = CG;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = CG == 2 ? 1 : 0;
+    cfg.numAttrs = CG == 2 ? 2 : 1;
     RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, (int)p.M, (int)p.N, (int)p.K, e));
     RF_TRY_LAUNCH("rf_gemm_kernel");
     return RF_OK;

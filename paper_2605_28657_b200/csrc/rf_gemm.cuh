@@ -12,9 +12,12 @@
 // main loop of tile i+1.  Tiles are walked m-fastest so CTAs running concurrently share
 // the same B (weight) tile through L2.
 #pragma once
+#include "rf_common.cuh"
 #include "rf_sm100.cuh"
 
 namespace rf::gemm {
+using ::rf::pdl_wait;
+using ::rf::pdl_launch;
 
 enum Epi : int {
     kStoreBF16 = 0,   // out(bf16)[m,n] = acc
@@ -132,6 +135,8 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();     // the previous kernel's outputs (A, the residual stream) are visible
+    pdl_launch();
 
     const int num_m = (M + TM - 1) / TM, num_n = N / BN, kblocks = K / BK;
     const int num_tiles = num_m * num_n;

@@ -424,10 +424,14 @@ class StreamPipeline:
                 self._step_slots(active)
             finished = [(i, s) for i, s in enumerate(self._slots)
                         if s is not None and s.step >= self.config.steps]
-            records = self._emit(finished) if finished else []
+            # emit: the statistics kernel and its read-back are queued, the finished slots
+            # are refilled (admission kernels queued behind them), and only then does the
+            # host wait for the device to build the records
+            pending = self._emit_launch(finished) if finished else None
             for i, _ in finished:
                 self._slots[i] = None
             self._refill()
+            records = self._emit_finish(finished, *pending) if finished else []
             self._prev_tick_denoise = self.denoise
             self._tick_index += 1
             return records
@@ -471,14 +475,28 @@ class StreamPipeline:
         T, D = cfg.shape
         jitter = self.model.perturbation
         draws, rows = [], []
-        for slot in slots:
+        if self.velocity_model is not None:
+            # the DiT's inputs first: its (long) batched forward is launched before the host
+            # prepares the solver rows, so that host work overlaps the device work
+            rows = [RfRow() for _ in slots]
+            for slot, row in zip(slots, rows):
+                base = slot.request.curves
+                need_uncond = (base.guidance_enabled and
+                               guidance_plan(base.rcfg_mode, slot.state, True)[0] == _native.RF_NEG_UNCOND)
+                self.velocity_model.prepare_row(self, slot, row, float(slot.schedule.sigmas[slot.step]),
+                                                need_uncond)
+            ev = self._phase_begin("model")
+            self.velocity_model.forward(self)
+            self._phase_end("model", ev)
+            self.launches_last_tick += getattr(self.velocity_model, "launches_per_forward", 0)
+        for i, slot in enumerate(slots):
             k = slot.step
             t_curr = float(slot.schedule.sigmas[k])
             t_next = float(slot.schedule.sigmas[k + 1])
             host, dev, base = self._curve_view(slot)
             req = slot.request
             nbuf = self._noise_buffers(slot)
-            row = RfRow()
+            row = RfRow() if self.velocity_model is None else rows[i]
             row.x = slot.x.data_ptr()
             row.t_curr, row.t_next = t_curr, t_next
             conds = req.conditions
@@ -495,11 +513,6 @@ class StreamPipeline:
                     draws.append((slot.rng.key(k, "model"), nbuf[0]))
                     row.noise_model = nbuf[0].data_ptr()
                     row.jitter_t = jitter * t_curr
-            else:
-                # the DiT computes every row of the tick in one batched forward (below)
-                need_uncond = (base.guidance_enabled and
-                               guidance_plan(base.rcfg_mode, slot.state, True)[0] == _native.RF_NEG_UNCOND)
-                self.velocity_model.prepare_row(self, slot, row, t_curr, need_uncond)
             curve_pointers(row, lambda n: dev[n])
             if base.guidance_enabled:
                 neg_kind, flags = guidance_plan(base.rcfg_mode, slot.state, True)
@@ -528,12 +541,8 @@ class StreamPipeline:
                 if host["ode_noise_curve"] is not None:
                     draws.append((slot.rng.key(k, "ode"), nbuf[1]))
                     row.noise_step = nbuf[1].data_ptr()
-            rows.append(row)
-        if self.velocity_model is not None:
-            ev = self._phase_begin("model")
-            self.velocity_model.forward(self)
-            self._phase_end("model", ev)
-            self.launches_last_tick += getattr(self.velocity_model, "launches_per_forward", 0)
+            if self.velocity_model is None:
+                rows.append(row)
         if draws:
             ev = self._phase_begin("noise")
             fill_normals(draws, self._status)
@@ -559,6 +568,10 @@ class StreamPipeline:
 
     def _emit(self, finished: list) -> list:
         """_emit for every finished slot, in slot-index order (pipeline.py:466-491)."""
+        return self._emit_finish(finished, *self._emit_launch(finished))
+
+    def _emit_launch(self, finished: list):
+        """Queue the emit statistics (isfinite, mse vs the last emitted / the reference)."""
         cfg = self.config
         n = len(finished)
         for _, slot in finished:
@@ -582,7 +595,14 @@ class StreamPipeline:
         self.launches_last_tick += 2
         self._stats_host.copy_(self._stats, non_blocking=True)
         self._status_host.copy_(self._status, non_blocking=True)
-        self._stream.synchronize()
+        done = torch.cuda.Event()
+        done.record(self._stream)
+        return recs_dev, done
+
+    def _emit_finish(self, finished: list, recs_dev: list, done) -> list:
+        """Wait for the statistics and build the CompletionRecords (pipeline.py:466-491)."""
+        cfg = self.config
+        done.synchronize()
         status = int(self._status_host[0])
         if status & _native.RF_STATUS_NONFINITE:
             raise RuntimeError("non-finite completion latent; aborting session")
