@@ -275,9 +275,24 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-template <int NH>
+// (x0, x1) * s + (c, c) with one packed FFMA2 (sm_100)
+__device__ __forceinline__ float2 fma2(float2 x, float s, float c) {
+    uint64_t r;
+    asm("{\n.reg .b64 a, b, d;\n"
+        "mov.b64 a, {%1, %2};\n"
+        "mov.b64 b, {%3, %3};\n"
+        "mov.b64 d, {%4, %4};\n"
+        "fma.rn.ftz.f32x2 %0, a, b, d;\n}"
+        : "=l"(r)
+        : "f"(x.x), "f"(x.y), "f"(s), "f"(c));
+    return make_float2(__uint_as_float((uint32_t)r), __uint_as_float((uint32_t)(r >> 32)));
+}
+
+
+
+template <int NH, int KVS>
 constexpr size_t fa_smem() {
-    return 1024 + (size_t)(NH + 2 + 2) * kOperand + 256;
+    return 1024 + (size_t)(NH + 2 * KVS) * kOperand + 256;
 }
 
 // debugging timeline ([cta][event][16] u64 clock64), set by rf_attn_set_trace; null in production
@@ -298,17 +313,19 @@ __device__ __forceinline__ unsigned long long globaltimer() {
             g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ev)) * 16 + (j)] = clock64(); \
     } while (0)
 
-template <int NH>
-__global__ void __launch_bounds__(128 * NH + 64, 1)
+// KVS = K/V stages: 2 (double-buffered) or 1 (one key tile, e.g. the cross-attention: the
+// CTA then fits twice per SM -- NH = 1, KVS = 1: 96 KB shared memory, 256 TMEM columns).
+template <int NH, int KVS>
+__global__ void __launch_bounds__(128 * NH + 64, (NH == 1 && KVS == 1) ? 2 : 1)
 rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tvt, __nv_bfloat16 *__restrict__ out, int64_t ldo, int Nq,
                   int Nk, int H, int Hkv, float scale_log2) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = base;                 // [NH]
-    uint8_t *sK = sQ + NH * kOperand;   // [2]
-    uint8_t *sV = sK + 2 * kOperand;    // [2] V^T tiles (rows = head dims, K-major over keys)
-    uint64_t *bar = (uint64_t *)(sV + 2 * kOperand);
+    uint8_t *sK = sQ + NH * kOperand;     // [KVS]
+    uint8_t *sV = sK + KVS * kOperand;    // [KVS] V^T tiles (rows = head dims, K-major over keys)
+    uint64_t *bar = (uint64_t *)(sV + KVS * kOperand);
     uint64_t *qfull = bar, *kfull = bar + 1, *kempty = bar + 3, *vfull = bar + 5, *vempty = bar + 7;
     uint64_t *sfull = bar + 9, *pfull = bar + 11, *odone = bar + 13;
     uint32_t *tmem_slot = (uint32_t *)(bar + 16);
@@ -355,8 +372,8 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
                 tma_load_2d(sQ + a * kOperand + kTile, &tq, qfull, (h0 + a) * 128 + 64, b * Nq + q0);
             }
             for (int j = 0; j < nt; ++j) {
-                const int s = j & 1;
-                const uint32_t ph = ((j >> 1) & 1) ^ 1;
+                const int s = j % KVS;
+                const uint32_t ph = ((j / KVS) & 1) ^ 1;
                 mbar_wait(&kempty[s], ph);
                 mbar_expect_tx(&kfull[s], kOperand);
                 tma_load_2d(sK + s * kOperand, &tk, &kfull[s], hk * 128, b * Nk + j * 128);
@@ -393,10 +410,10 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             for (int a = 0; a < NH; ++a) mma_s(a, 0);
             umma_commit(&kempty[0]);
             for (int j = 0; j < nt; ++j) {
-                const int s = j & 1, s1 = (j + 1) & 1;
+                const int s = j % KVS, s1 = (j + 1) % KVS;
                 for (int a = 0; a < NH; ++a) {
                     mbar_wait(&pfull[a], j & 1);
-                    if (a == 0) mbar_wait(&vfull[s], (j >> 1) & 1);
+                    if (a == 0) mbar_wait(&vfull[s], (j / KVS) & 1);
                     tc_fence_after();
                     FA_TRACE(a, j);
                     mma_o(a, s, j > 0);
@@ -404,7 +421,7 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
                     if (j + 1 < nt) {
                         // no wait for PV_a(j): tcgen05.mma executes in issue order, so S_a(j+1)
                         // cannot overwrite the P_a(j) columns before PV_a(j) has read them
-                        if (a == 0) mbar_wait(&kfull[s1], ((j + 1) >> 1) & 1);
+                        if (a == 0) mbar_wait(&kfull[s1], ((j + 1) / KVS) & 1);
                         tc_fence_after();
                         FA_TRACE(2 + a, j + 1);
                         mma_s(a, s1);
@@ -471,10 +488,12 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
                 float ls = 0.f;
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                    const float p0 = ex2_approx(fmaf(__uint_as_float(r[c * 32 + 2 * e]), scale_log2, nm));
-                    const float p1 = ex2_approx(fmaf(__uint_as_float(r[c * 32 + 2 * e + 1]), scale_log2, nm));
-                    ls += p0 + p1;
-                    __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
+                    const float2 x = fma2(make_float2(__uint_as_float(r[c * 32 + 2 * e]),
+                                                      __uint_as_float(r[c * 32 + 2 * e + 1])),
+                                          scale_log2, nm);
+                    const float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                    ls += pv.x + pv.y;
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(pv.x, pv.y);
                     pk[e] = *(uint32_t *)&hh;
                 }
                 l += ls;
@@ -537,17 +556,17 @@ int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const voi
     return rc;
 }
 
-template <int NH>
+template <int NH, int KVS>
 static int launch_fa(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)fa_smem<NH>()));
+        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa_kernel<NH, KVS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fa_smem<NH, KVS>()));
         attr = true;
     }
     dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / NH);
-    RF_TRY_CUDA(launch_pdl(rf_attn_fa_kernel<NH>, grid, dim3(128 * NH + 64), fa_smem<NH>(), st, p.tq, p.tk, p.tvt,
-                           (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
+    RF_TRY_CUDA(launch_pdl(rf_attn_fa_kernel<NH, KVS>, grid, dim3(128 * NH + 64), fa_smem<NH, KVS>(), st, p.tq, p.tk,
+                           p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
     RF_TRY_LAUNCH("rf_attn_fa_kernel");
     return RF_OK;
 }
@@ -556,7 +575,12 @@ int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) 
     const bool pair = (p.H / p.Hkv) % 2 == 0;   // two query heads share each KV head
     const float sc = 1.4426950408889634f / sqrtf(128.f);
     static const bool two_pass = getenv("RF_ATTN_TWO_PASS") != nullptr;   // the earlier two-pass kernel
-    if (!two_pass) return pair ? launch_fa<2>(p, out, ldo, B, sc, st) : launch_fa<1>(p, out, ldo, B, sc, st);
+    if (!two_pass) {
+        // one key tile (cross-attention to 128 conditioning tokens): one head per CTA, two CTAs
+        // per SM; longer key ranges: the GQA head pair ping-pongs inside one CTA
+        if (p.Nk <= kTcRows) return launch_fa<1, 1>(p, out, ldo, B, sc, st);
+        return pair ? launch_fa<2, 2>(p, out, ldo, B, sc, st) : launch_fa<1, 2>(p, out, ldo, B, sc, st);
+    }
     if (pair) {
         static bool attr = false;
         if (!attr) {
