@@ -290,12 +290,42 @@ __device__ __forceinline__ float2 fma2(float2 x, float s, float c) {
 
 
 
+// 2^x for a pair on the FMA pipe (x <= 8 or -inf): round-to-nearest split x = j + f with
+// f in [-1/2, 1/2] (magic-number add), 2^f by a degree-3 polynomial (max rel. error 7.7e-5,
+// far below P's bf16 step of 3.9e-3), j added to the exponent bits with one integer
+// multiply-add.  The MUFU ex2 unit (16 / clk / SM) is the softmax's bottleneck; computing a
+// share of the exponentials here balances the two pipes.
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    return (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(b) << 32);
+}
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+    constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer
+    const float x0 = fmaxf(x.x, -125.f), x1 = fmaxf(x.y, -125.f);
+    uint64_t t, j, f, p;
+    asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk2(x0, x1)), "l"(pk2(kMagic, kMagic)));
+    asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(j) : "l"(t), "l"(pk2(kMagic, kMagic)));
+    asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(f) : "l"(pk2(x0, x1)), "l"(j));
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f), "l"(pk2(0.05508868f, 0.05508868f)),
+        "l"(pk2(0.24260405f, 0.24260405f)));
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f), "l"(p), "l"(pk2(0.69327624f, 0.69327624f)));
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f), "l"(p), "l"(pk2(0.99992894f, 0.99992894f)));
+    const uint32_t r0 = (uint32_t)t * (1u << 23) + (uint32_t)p;
+    const uint32_t r1 = (uint32_t)(t >> 32) * (1u << 23) + (uint32_t)(p >> 32);
+    return make_float2(__uint_as_float(r0), __uint_as_float(r1));
+}
+
+constexpr int kPolyPairs = 6;   // of 16 exponential pairs per 32-column chunk (see exp2_poly2)
+
+// NH = 2: three full warpgroups (two softmax groups + one with the MMA and TMA warps) so
+// registers can be moved between them with setmaxnreg; NH = 1: softmax group + 2 warps.
+constexpr int fa_threads(int nh) { return nh == 2 ? 384 : 128 * nh + 64; }
+
 template <int NH, int KVS>
 constexpr size_t fa_smem() {
     return 1024 + (size_t)(NH + 2 * KVS) * kOperand + 256;
 }
 
-// debugging timeline ([cta][event][16] u64 clock64), set by rf_attn_set_trace; null in production
+// debugging timeline ([cta][16 events][16] u64 clock64), set by rf_attn_set_trace; null in production
 __device__ unsigned long long *g_attn_trace = nullptr;
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -305,18 +335,19 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 #define FA_GTRACE(ev)                                                                                     \
     do {                                                                                                  \
         if (g_attn_trace)                                                                                 \
-            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ev)) * 16 + 15] = globaltimer(); \
+            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)) * 16 + 15] = globaltimer(); \
     } while (0)
 #define FA_TRACE(ev, j)                                                                                  \
     do {                                                                                                 \
         if (g_attn_trace && (j) < 16)                                                                    \
-            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 8 + (ev)) * 16 + (j)] = clock64(); \
+            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)) * 16 + (j)] = clock64(); \
     } while (0)
 
 // KVS = K/V stages: 2 (double-buffered) or 1 (one key tile, e.g. the cross-attention: the
 // CTA then fits twice per SM -- NH = 1, KVS = 1: 96 KB shared memory, 256 TMEM columns).
-template <int NH, int KVS>
-__global__ void __launch_bounds__(128 * NH + 64, (NH == 1 && KVS == 1) ? 2 : 1)
+// PE = exponential pairs (of every 16) computed by exp2_poly2 instead of MUFU ex2.
+template <int NH, int KVS, int PE, bool PP>
+__global__ void __launch_bounds__(fa_threads(NH), (NH == 1 && KVS == 1) ? 2 : 1)
 rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tvt, __nv_bfloat16 *__restrict__ out, int64_t ldo, int Nq,
                   int Nk, int H, int Hkv, float scale_log2) {
@@ -332,7 +363,6 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int MMA_WARP = 4 * NH, TMA_WARP = 4 * NH + 1;
-    if (tid == 0) FA_GTRACE(0);
     const int group = H / Hkv;
     const int bh = blockIdx.y, per_b = H / NH, b = bh / per_b, h0 = (bh % per_b) * NH;
     const int hk = h0 / group;
@@ -363,8 +393,12 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     const uint32_t tmem = *tmem_slot;
     pdl_wait();
     pdl_launch();
-
-    if (warp == TMA_WARP) {
+    if (tid == 0) FA_GTRACE(0);
+    // NH = 2: the softmax threads hold a whole 128-column S row in registers; setmaxnreg gives
+    // them the registers the MMA / TMA warpgroup does not need (the CTA pool is 384 x 168 at launch: 8 x 200 + 4 x 96 warps fit)
+    if (warp >= MMA_WARP) {
+      if constexpr (NH == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
+      if (warp == TMA_WARP) {
         if (elect_one()) {
             mbar_expect_tx(qfull, NH * kOperand);
             for (int a = 0; a < NH; ++a) {
@@ -384,7 +418,7 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
                 tma_load_2d(sV + s * kOperand + kTile, &tvt, &vfull[s], j * 128 + 64, (b * Hkv + hk) * 128);
             }
         }
-    } else if (warp == MMA_WARP) {
+      } else if (warp == MMA_WARP) {
         if (elect_one()) {
             auto mma_s = [&](int a, int s) {   // S_a = Q_a K_s^T
 #pragma unroll
@@ -430,7 +464,9 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
                 }
             }
         }
+      }
     } else {
+        if constexpr (NH == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
         // softmax warps: thread owns query row `row` of head a
         const int a = warp >> 2, quarter = warp & 3;
         const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
@@ -438,6 +474,14 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         float m = 0.f, l = 0.f;
         for (int j = 0; j < nt; ++j) {
             mbar_wait(&sfull[a], j & 1);
+            if constexpr (PP && NH == 2) {
+                // strict ping-pong: head 1's softmax of tile j starts when head 0's has
+                // finished, head 0's of tile j + 1 when head 1's of tile j has -- the two
+                // softmax groups take turns on the exp/issue pipes while the tensor core
+                // works for the other head
+                if (a == 1) mbar_wait(&pfull[0], j & 1);
+                else if (j > 0) mbar_wait(&pfull[1], (j - 1) & 1);
+            }
             tc_fence_after();
             if (quarter == 0 && lane == 0) FA_TRACE(4 + a, j);
             const int valid = Nk - j * 128;
@@ -447,14 +491,21 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             tmem_ld32(tS + 64, *(uint32_t(*)[32])(r + 64));
             tmem_ld32(tS + 96, *(uint32_t(*)[32])(r + 96));
             tmem_ld_wait();
+            if (quarter == 0 && lane == 0) FA_TRACE(8 + a, j);
             if (valid < 128) {   // the last key tile: keys >= valid are masked
 #pragma unroll
                 for (int e = 0; e < 128; ++e)
                     if (e >= valid) r[e] = __float_as_uint(-INFINITY);
             }
-            float tmax = -INFINITY;
+            // row max as 4 independent 3-input max chains (a single chain is 64 dependent ops)
+            float mx[4];
 #pragma unroll
-            for (int e = 0; e < 128; e += 2) tmax = fmaxf(tmax, fmaxf(__uint_as_float(r[e]), __uint_as_float(r[e + 1])));
+            for (int q = 0; q < 4; ++q) mx[q] = fmaxf(__uint_as_float(r[q]), __uint_as_float(r[q + 4]));
+#pragma unroll
+            for (int e = 8; e < 128; e += 8)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], fmaxf(__uint_as_float(r[e + q]), __uint_as_float(r[e + q + 4])));
+            float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
             tmax *= scale_log2;
             if (j == 0) {
                 m = tmax;
@@ -482,23 +533,25 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             // needs no range fix-up.  l sums the fp32 values (the bf16 rounding of P is below
             // the output's own bf16 step).
             const float nm = -m;
+            if (quarter == 0 && lane == 0) FA_TRACE(10 + a, j);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t pk[16];
-                float ls = 0.f;
+                uint64_t ls = 0;   // packed (even, odd) partial sums
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const float2 x = fma2(make_float2(__uint_as_float(r[c * 32 + 2 * e]),
                                                       __uint_as_float(r[c * 32 + 2 * e + 1])),
                                           scale_log2, nm);
-                    const float2 pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                    ls += pv.x + pv.y;
+                    const float2 pv = e < PE ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                    asm("add.rn.ftz.f32x2 %0, %0, %1;" : "+l"(ls) : "l"(pk2(pv.x, pv.y)));
                     __nv_bfloat162 hh = __floats2bfloat162_rn(pv.x, pv.y);
                     pk[e] = *(uint32_t *)&hh;
                 }
-                l += ls;
+                l += __uint_as_float((uint32_t)ls) + __uint_as_float((uint32_t)(ls >> 32));
                 tmem_st16(tS + c * 16, pk);
             }
+            if (quarter == 0 && lane == 0) FA_TRACE(12 + a, j);
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -537,6 +590,257 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     if (warp == MMA_WARP) tmem_dealloc<256 * NH>(tmem);
 }
 
+// ---------------------------------------------------------------------------------
+// Self-attention over 64-key tiles with double-buffered scores (the default when the GQA
+// head pair shares a KV head and there is more than one 128-key tile).
+//
+// CTA = one 128-row query tile x the 2 query heads of one KV head; 12 warps: warpgroup a
+// (a = 0, 1) runs head a's softmax (one query row per thread), warp 8 issues the MMAs,
+// warp 9 the TMA loads.  Per head, S_j = Q K_j^T (M=128, N=64) goes into one of two
+// 64-column TMEM buffers, so S_{j+1} is computed while the softmax works on S_j: the
+// tensor core never waits for the softmax and the softmax never waits for a fresh S.
+// P_j (bf16) overwrites the first 32 columns of its S buffer and O += P_j V_j reads it
+// from TMEM (TS MMA, V^T tile K-major over keys).  MMA order per head:
+// ... PV(j-1), S(j+1), PV(j), S(j+2) ... -- tcgen05 executes in issue order, so S(j+2)
+// cannot overwrite P(j) before PV(j) has read it.  Running max with lazy O rescaling
+// (only when the tile max grows by more than 2^8; the softmax first waits for PV(j-1)).
+// TMEM: head a: S buffers at columns a*128 + {0, 64}, O at 256 + a*128 (512 total).
+// K / V^T tiles: KS-stage rings of 16 KB each.
+constexpr int kKeys64 = 64;
+constexpr int kFa64Stages = 4;
+constexpr uint32_t kK64Half = 64 * 64 * 2;        // [64 keys][64 dims] bf16, SW128
+constexpr uint32_t kK64Tile = 2 * kK64Half;       // [64 keys][128 dims]
+constexpr uint32_t kV64Tile = 128 * 64 * 2;       // [128 dims][64 keys]
+constexpr size_t fa64_smem() { return 1024 + 2 * (size_t)kOperand + kFa64Stages * (size_t)(kK64Tile + kV64Tile) + 256; }
+
+template <int PE>
+__global__ void __launch_bounds__(384, 1)
+rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                    const __grid_constant__ CUtensorMap tvt, __nv_bfloat16 *__restrict__ out, int64_t ldo, int Nq,
+                    int Nk, int H, int Hkv, float scale_log2) {
+    constexpr int KS = kFa64Stages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sQ = base;                    // [2 heads] x 32 KB
+    uint8_t *sK = sQ + 2 * kOperand;       // [KS] x 16 KB
+    uint8_t *sV = sK + KS * kK64Tile;      // [KS] x 16 KB (V^T: rows = head dims)
+    uint64_t *bar = (uint64_t *)(sV + KS * kV64Tile);
+    uint64_t *qfull = bar, *kfull = bar + 1, *kempty = kfull + KS, *vfull = kempty + KS, *vempty = vfull + KS;
+    uint64_t *sfull = vempty + KS;         // [head * 2 + buffer]
+    uint64_t *pfull = sfull + 4, *odone = pfull + 2;
+    uint32_t *tmem_slot = (uint32_t *)(odone + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int MMA_WARP = 8, TMA_WARP = 9;
+    const int group = H / Hkv;
+    const int bh = blockIdx.y, per_b = H / 2, b = bh / per_b, h0 = (bh % per_b) * 2;
+    const int hk = h0 / group;
+    const int q0 = blockIdx.x * kTcRows;
+    const int nt = (Nk + kKeys64 - 1) / kKeys64;
+    constexpr uint32_t idesc_s = idesc_bf16(128, 64), idesc_o = idesc_bf16(128, 128);
+
+    if (tid == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tk);
+        tma_prefetch(&tvt);
+        mbar_init(qfull, 1);
+        for (int i = 0; i < KS; ++i) {
+            mbar_init(&kfull[i], 1);
+            mbar_init(&kempty[i], 1);
+            mbar_init(&vfull[i], 1);
+            mbar_init(&vempty[i], 1);
+        }
+        for (int i = 0; i < 4; ++i) mbar_init(&sfull[i], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&pfull[i], 4);   // the 4 softmax warps of the head
+            mbar_init(&odone[i], 1);
+        }
+        mbar_fence_init();
+    }
+    if (warp == MMA_WARP) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_launch();
+    if (tid == 0) FA_GTRACE(0);
+
+    if (warp == TMA_WARP) {
+        if (elect_one()) {
+            mbar_expect_tx(qfull, 2 * kOperand);
+            for (int a = 0; a < 2; ++a) {
+                tma_load_2d(sQ + a * kOperand, &tq, qfull, (h0 + a) * 128, b * Nq + q0);
+                tma_load_2d(sQ + a * kOperand + kTile, &tq, qfull, (h0 + a) * 128 + 64, b * Nq + q0);
+            }
+            for (int j = 0; j < nt; ++j) {
+                const int s = j % KS;
+                const uint32_t ph = ((j / KS) & 1) ^ 1;
+                mbar_wait(&kempty[s], ph);
+                mbar_expect_tx(&kfull[s], kK64Tile);
+                tma_load_2d(sK + s * kK64Tile, &tk, &kfull[s], hk * 128, b * Nk + j * kKeys64);
+                tma_load_2d(sK + s * kK64Tile + kK64Half, &tk, &kfull[s], hk * 128 + 64, b * Nk + j * kKeys64);
+                mbar_wait(&vempty[s], ph);
+                mbar_expect_tx(&vfull[s], kV64Tile);
+                tma_load_2d(sV + s * kV64Tile, &tvt, &vfull[s], j * kKeys64, (b * Hkv + hk) * 128);
+            }
+        }
+    } else if (warp == MMA_WARP) {
+        if (elect_one()) {
+            auto mma_s = [&](int a, int s, int buf) {   // S_a -> buffer buf
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t ad = sdesc_sw128(sQ + a * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
+                    const uint64_t bd = sdesc_sw128(sK + s * kK64Tile + (ks >> 2) * kK64Half) + (uint64_t)((ks & 3) * 2);
+                    umma_bf16(tmem + a * 128 + buf * 64, ad, bd, idesc_s, ks > 0);
+                }
+                umma_commit(&sfull[a * 2 + buf]);
+            };
+            auto mma_o = [&](int a, int s, int buf, bool acc) {   // O_a += P_a V (P in TMEM)
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const uint64_t bd = sdesc_sw128(sV + s * kV64Tile) + (uint64_t)(ks * 2);
+                    umma_bf16_ts(tmem + 256 + a * 128, tmem + a * 128 + buf * 64 + ks * 8, bd, idesc_o,
+                                 (acc || ks > 0) ? 1u : 0u);
+                }
+                umma_commit(&odone[a]);
+            };
+            mbar_wait(qfull, 0);
+            for (int j = 0; j < 2 && j < nt; ++j) {
+                mbar_wait(&kfull[j], 0);
+                tc_fence_after();
+                mma_s(0, j, j);
+                mma_s(1, j, j);
+                umma_commit(&kempty[j]);
+            }
+            for (int j = 0; j < nt; ++j) {
+                const int s = j % KS, s2 = (j + 2) % KS, buf = j & 1;
+#pragma unroll 1
+                for (int a = 0; a < 2; ++a) {
+                    mbar_wait(&pfull[a], j & 1);
+                    if (a == 0) mbar_wait(&vfull[s], (j / KS) & 1);
+                    tc_fence_after();
+                    FA_TRACE(a, j);
+                    mma_o(a, s, buf, j > 0);
+                    if (a == 1) umma_commit(&vempty[s]);
+                    if (j + 2 < nt) {
+                        if (a == 0) mbar_wait(&kfull[s2], ((j + 2) / KS) & 1);
+                        tc_fence_after();
+                        FA_TRACE(2 + a, j + 2);
+                        mma_s(a, s2, buf);
+                        if (a == 1) umma_commit(&kempty[s2]);
+                    }
+                }
+            }
+        }
+    } else if (warp < MMA_WARP) {
+        const int a = warp >> 2, quarter = warp & 3;
+        const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+        const uint32_t tO = tmem + lane_base + 256 + a * 128;
+        float m = 0.f, l = 0.f;
+        for (int j = 0; j < nt; ++j) {
+            const int buf = j & 1;
+            const uint32_t tS = tmem + lane_base + a * 128 + buf * 64;
+            mbar_wait(&sfull[a * 2 + buf], (j >> 1) & 1);
+            tc_fence_after();
+            if (quarter == 0 && lane == 0) FA_TRACE(4 + a, j);
+            uint32_t r[64];
+            tmem_ld32(tS, *(uint32_t(*)[32])(r));
+            tmem_ld32(tS + 32, *(uint32_t(*)[32])(r + 32));
+            tmem_ld_wait();
+            const int valid = Nk - j * kKeys64;
+            if (valid < kKeys64) {   // the last key tile: keys >= valid are masked
+#pragma unroll
+                for (int e = 0; e < 64; ++e)
+                    if (e >= valid) r[e] = __float_as_uint(-INFINITY);
+            }
+            float mx[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mx[q] = fmaxf(__uint_as_float(r[q]), __uint_as_float(r[q + 4]));
+#pragma unroll
+            for (int e = 8; e < 64; e += 8)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], fmaxf(__uint_as_float(r[e + q]), __uint_as_float(r[e + q + 4])));
+            const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+            if (j == 0) {
+                m = tmax;
+            } else {
+                mbar_wait(&odone[a], (j - 1) & 1);   // PV(j-1) done: O stable (and phases tracked exactly)
+                const bool need = tmax > m + 8.f;
+                if (__any_sync(0xffffffffu, need)) {   // lazy rescale of O and l
+                    tc_fence_after();
+                    const float mn = need ? tmax : m;
+                    const float f = ex2_approx(m - mn);
+                    l *= f;
+                    m = mn;
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                        tmem_st32(tO + c * 32, o);
+                    }
+                    tmem_st_wait();
+                }
+            }
+            const float nm = -m;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t pk[16];
+                uint64_t ls = 0;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const float2 x = fma2(make_float2(__uint_as_float(r[c * 32 + 2 * e]),
+                                                      __uint_as_float(r[c * 32 + 2 * e + 1])),
+                                          scale_log2, nm);
+                    const float2 pv = e < PE ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                    asm("add.rn.ftz.f32x2 %0, %0, %1;" : "+l"(ls) : "l"(pk2(pv.x, pv.y)));
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(pv.x, pv.y);
+                    pk[e] = *(uint32_t *)&hh;
+                }
+                l += __uint_as_float((uint32_t)ls) + __uint_as_float((uint32_t)(ls >> 32));
+                tmem_st16(tS + c * 16, pk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[a]);
+            if (quarter == 0 && lane == 0) FA_TRACE(6 + a, j);
+        }
+        mbar_wait(&odone[a], (nt - 1) & 1);
+        tc_fence_after();
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        const int qrow = q0 + quarter * 32 + lane;
+        const int h = h0 + a;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tO + c * 32, r);
+            tmem_ld_wait();
+            if (qrow < Nq) {
+                __nv_bfloat16 *dst = out + ((int64_t)b * Nq + qrow) * ldo + h * 128 + c * 32;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]) * inv_l,
+                                                                  __uint_as_float(r[q * 8 + 2 * e + 1]) * inv_l);
+                        w[e] = *(uint32_t *)&hh;
+                    }
+                    *(uint4 *)(dst + q * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) FA_GTRACE(1);
+    if (warp == MMA_WARP) tmem_dealloc<512>(tmem);
+}
+
 int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const void *k, int64_t ldk, int64_t k_cols,
               const void *vt, int B, int Nq, int Nk, int Nk_pad, int H, int Hkv) {
     if (H % Hkv || Nk_pad % 8 || Nk > Nk_pad) {
@@ -547,6 +851,7 @@ int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const voi
     if (!rc) rc = make_tmap_bf16_2d(&p->tk, k, (uint64_t)k_cols, (uint64_t)B * Nk, (uint64_t)ldk * 2, 64, 128);
     if (!rc)
         rc = make_tmap_bf16_2d(&p->tvt, vt, (uint64_t)Nk_pad, (uint64_t)B * Hkv * 128, (uint64_t)Nk_pad * 2, 64, 128);
+    if (!rc) rc = make_tmap_bf16_2d(&p->tk64, k, (uint64_t)k_cols, (uint64_t)B * Nk, (uint64_t)ldk * 2, 64, 64);
     p->B = B;
     p->Nq = Nq;
     p->Nk = Nk;
@@ -556,19 +861,60 @@ int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const voi
     return rc;
 }
 
-template <int NH, int KVS>
-static int launch_fa(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+template <int NH, int KVS, int PE, bool PP>
+static int launch_fa_pp(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa_kernel<NH, KVS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)fa_smem<NH, KVS>()));
+        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa_kernel<NH, KVS, PE, PP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_smem<NH, KVS>()));
         attr = true;
     }
     dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / NH);
-    RF_TRY_CUDA(launch_pdl(rf_attn_fa_kernel<NH, KVS>, grid, dim3(128 * NH + 64), fa_smem<NH, KVS>(), st, p.tq, p.tk,
-                           p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
+    RF_TRY_CUDA(launch_pdl(rf_attn_fa_kernel<NH, KVS, PE, PP>, grid, dim3(fa_threads(NH)), fa_smem<NH, KVS>(), st,
+                           p.tq, p.tk, p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
     RF_TRY_LAUNCH("rf_attn_fa_kernel");
     return RF_OK;
+}
+
+template <int NH, int KVS, int PE>
+static int launch_fa_pe(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+    static const bool pp = getenv("RF_ATTN_PP") ? atoi(getenv("RF_ATTN_PP")) != 0 : true;
+    if (NH == 2 && pp) return launch_fa_pp<NH, KVS, PE, true>(p, out, ldo, B, sc, st);
+    return launch_fa_pp<NH, KVS, PE, false>(p, out, ldo, B, sc, st);
+}
+
+static int poly_pairs() {   // RF_ATTN_POLY overrides the share of FMA-pipe exponentials (tuning aid)
+    static const int v = [] {
+        const char *e = getenv("RF_ATTN_POLY");
+        return e ? atoi(e) : kPolyPairs;
+    }();
+    return v;
+}
+
+template <int PE>
+static int launch_fa64(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa64_kernel<PE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fa64_smem()));
+        attr = true;
+    }
+    dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / 2);
+    RF_TRY_CUDA(launch_pdl(rf_attn_fa64_kernel<PE>, grid, dim3(384), fa64_smem(), st, p.tq, p.tk64, p.tvt,
+                           (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
+    RF_TRY_LAUNCH("rf_attn_fa64_kernel");
+    return RF_OK;
+}
+
+template <int NH, int KVS>
+static int launch_fa(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+    switch (poly_pairs()) {
+        case 0: return launch_fa_pe<NH, KVS, 0>(p, out, ldo, B, sc, st);
+        case 4: return launch_fa_pe<NH, KVS, 4>(p, out, ldo, B, sc, st);
+        case 6: return launch_fa_pe<NH, KVS, 6>(p, out, ldo, B, sc, st);
+        case 8: return launch_fa_pe<NH, KVS, 8>(p, out, ldo, B, sc, st);
+        default: return launch_fa_pe<NH, KVS, 10>(p, out, ldo, B, sc, st);
+    }
 }
 
 int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) {
@@ -579,6 +925,14 @@ int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) 
         // one key tile (cross-attention to 128 conditioning tokens): one head per CTA, two CTAs
         // per SM; longer key ranges: the GQA head pair ping-pongs inside one CTA
         if (p.Nk <= kTcRows) return launch_fa<1, 1>(p, out, ldo, B, sc, st);
+        static const int fa64 = getenv("RF_ATTN_FA64") ? atoi(getenv("RF_ATTN_FA64")) : 1;
+        if (pair && fa64) {
+            switch (poly_pairs()) {
+                case 0: return launch_fa64<0>(p, out, ldo, B, sc, st);
+                case 4: return launch_fa64<4>(p, out, ldo, B, sc, st);
+                default: return launch_fa64<6>(p, out, ldo, B, sc, st);
+            }
+        }
         return pair ? launch_fa<2, 2>(p, out, ldo, B, sc, st) : launch_fa<1, 2>(p, out, ldo, B, sc, st);
     }
     if (pair) {

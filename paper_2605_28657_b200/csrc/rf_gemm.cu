@@ -57,10 +57,10 @@ static int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dt, const void *pt
     return RF_OK;
 }
 
-template <int BN, int EPI, int CG>
+template <int BN, int EPI, int CG, int CC = BN>
 static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
-    using C = gemm::Cfg<BN, CG, EPI>;
-    auto kern = gemm::rf_gemm_kernel<BN, EPI, CG>;
+    using C = gemm::Cfg<BN, CG, EPI, CC>;
+    auto kern = gemm::rf_gemm_kernel<BN, EPI, CG, CC>;
     static bool attr = false;
     if (!attr) {
         RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -93,7 +93,10 @@ static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStre
     switch (epi) {
         case gemm::kStoreBF16: return launch<BN, gemm::kStoreBF16, CG>(p, e, st);
         case gemm::kStoreF32: return launch<BN, gemm::kStoreF32, CG>(p, e, st);
-        case gemm::kResidGate: return launch<BN, gemm::kResidGate, CG>(p, e, st);
+        case gemm::kResidGate:
+            // long K: the main loop hides a two-pass residual epilogue; keep the operand stages
+            if (BN == 128 && p.K >= 4096) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
+            return launch<BN, gemm::kResidGate, CG>(p, e, st);
         case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG>(p, e, st);
         case gemm::kStoreF32Scale: return launch<BN, gemm::kStoreF32Scale, CG>(p, e, st);
         case gemm::kBF16Rope: return launch<BN, gemm::kBF16Rope, CG>(p, e, st);

@@ -52,6 +52,17 @@ struct EpiArgs {
     unsigned long long *trace;
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// globaltimer (ns) stamps: kernel entry -> [cta][15][7], exit -> [cta][14][7]
+#define RF_GTRACE(tile)                                                                          \
+    do {                                                                                         \
+        if (epi.trace && threadIdx.x == 0) epi.trace[((size_t)blockIdx.x * 16 + (tile)) * 8 + 7] = gtimer(); \
+    } while (0)
+
 #define RF_TRACE(tile, slot)                                                                          \
     do {                                                                                              \
         if (epi.trace && (tile) < 16)                                                                 \
@@ -68,15 +79,18 @@ constexpr int BM = 128, BK = 64;
 // fp32 slice of the residual stream into shared memory with TMA (issued before the
 // accumulator is ready, so the read overlaps the main loop), updates it in place from TMEM,
 // and writes it back with a TMA store -- instead of row-per-thread global loads/stores.
-template <int BN, int CG = 1, int EPI = 0>
+// CC: residual columns staged per pass (BN: one pass per tile; 64: two passes, half the
+// staging memory, two more operand stages -- for long K, where the main loop hides the
+// epilogue anyway and latency tolerance matters more).
+template <int BN, int CG = 1, int EPI = 0, int CC = BN>
 struct Cfg {
     static constexpr int BN_LOAD = BN / CG;   // B rows staged by each CTA
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN_LOAD * BK * 2;
     static constexpr bool TMA_C = EPI == 2 && BN == 128;
-    static constexpr int C_COLS = 64;                                           // staged per pass
+    static constexpr int C_COLS = CC;                                           // staged per pass
     static constexpr uint32_t C_WARP_BYTES = TMA_C ? 32u * C_COLS * 4u : 0u;   // per epilogue warp
-    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES;
+    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + (TMA_C ? 4u * 1024u : 0u);   // + gate rows
     // as many operand stages as fit next to the epilogue staging (227 KB opt-in limit)
     static constexpr uint32_t BUDGET = 232448u - 1024u - 512u - C_BYTES;
     static constexpr int STAGES = (int)(BUDGET / (A_BYTES + B_BYTES)) > 10 ? 10 : (int)(BUDGET / (A_BYTES + B_BYTES));
@@ -85,12 +99,12 @@ struct Cfg {
 
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
 
-template <int BN, int EPI, int CG = 1>
+template <int BN, int EPI, int CG = 1, int CC = BN>
 __global__ void __launch_bounds__(192, 1)
 rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, EpiArgs epi) {
     using namespace rf::sm100;
-    using C = Cfg<BN, CG, EPI>;
+    using C = Cfg<BN, CG, EPI, CC>;
     constexpr int TM = BM * CG;   // output rows per tile (per CTA pair when CG = 2)
     constexpr int STAGES = C::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -105,6 +119,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     uint64_t *cfull = tempty + 2;            // [4] one per epilogue warp (TMA_C)
     uint32_t *tmem_slot = (uint32_t *)(cfull + 4);
 
+    RF_GTRACE(15);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;   // 0 = leader (issues the MMAs)
     if (warp == 0 && lane == 0) {
@@ -137,6 +152,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     const uint32_t tmem = *tmem_slot;
     pdl_wait();     // the previous kernel's outputs (A, the residual stream) are visible
     pdl_launch();
+    RF_GTRACE(13);
 
     const int num_m = (M + TM - 1) / TM, num_n = N / BN, kblocks = K / BK;
     const int num_tiles = num_m * num_n;
@@ -219,70 +235,87 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             }
         }
     } else if constexpr (C::TMA_C) {
-        // gated residual, TMA-staged: out[m, n] += gate[m / rows_per_batch, n] * acc
+        // gated residual, TMA-staged: out[m, n] += gate[m / rows_per_batch, n] * acc.  Each
+        // epilogue warp owns a [32 rows][CC] fp32 slice of the residual stream in shared
+        // memory per pass: loaded by TMA while the main loop runs (the next pass's slice is
+        // requested as soon as the previous store has read the buffer), updated in place
+        // from TMEM, written back with one TMA store per 32-column box.  The two gate rows
+        // a 32-row slice can touch are staged in shared memory before the accumulator is
+        // ready, and the accumulator is released before the last store.
         const int q = warp & 3;
-        uint8_t *sw = sC + q * C::C_WARP_BYTES;   // C_COLS/32 boxes of [32 rows][32 fp32], SWIZZLE_128B
-        constexpr int NB = C::C_COLS / 32;
+        uint8_t *sw = sC + q * C::C_WARP_BYTES;   // NB boxes of [32 rows][32 fp32], SWIZZLE_128B
+        float *gs = (float *)(sC + 4 * C::C_WARP_BYTES + q * 1024);   // [2][BN] gate rows
+        constexpr int NB = CC / 32, NP = BN / CC;
+        static_assert(BN == 128 && NB * 32 * NP == BN, "residual epilogue shape");
+        auto tile_m0 = [&](int t) { return (t % num_m) * TM + (int)rank * BM + q * 32; };
+        auto tile_n0 = [&](int t) { return (t / num_m) * BN; };
+        auto load_pass = [&](int t, int p) {
+            mbar_expect_tx(&cfull[q], C::C_WARP_BYTES);
+#pragma unroll
+            for (int j = 0; j < NB; ++j)
+                tma_load_2d(sw + j * 4096, &tma_c, &cfull[q], tile_n0(t) + p * CC + j * 32, tile_m0(t));
+        };
         int acc = 0, it = 0;
         uint32_t acc_phase = 0, c_phase = 0;
+        if (lane == 0 && unit < num_tiles) load_pass(unit, 0);
         for (int t = unit; t < num_tiles; t += units, ++it) {
-            const int m0 = (t % num_m) * TM + (int)rank * BM + q * 32, n0 = (t / num_m) * BN;
-            const int m = m0 + lane;
-            const float *g = epi.gate + (int64_t)(min(m, M - 1) / epi.rows_per_batch) * epi.gate_ld + n0;
-            if (lane == 0)   // later passes' residual slices -> L2 now, so their loads below are L2 hits
-                for (int j = NB; j < BN / 32; ++j) tma_prefetch_l2_2d(&tma_c, n0 + j * 32, m0);
+            const int m0 = tile_m0(t), n0 = tile_n0(t);
+            const int m = min(m0 + lane, M - 1);
+            const int b_lo = min(m0, M - 1) / epi.rows_per_batch, b_hi = min(m0 + 31, M - 1) / epi.rows_per_batch;
+            __syncwarp();   // the previous tile's gate reads are done
+            ((float4 *)gs)[lane] = __ldg((const float4 *)(epi.gate + (int64_t)b_lo * epi.gate_ld + n0) + lane);
+            ((float4 *)gs)[32 + lane] = __ldg((const float4 *)(epi.gate + (int64_t)b_hi * epi.gate_ld + n0) + lane);
+            __syncwarp();
+            const float *gr = gs + (m / epi.rows_per_batch != b_lo ? BN : 0);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            if (q == 2 && lane == 0) RF_TRACE(it, 4);
 #pragma unroll 1
-            for (int p0 = 0; p0 < BN; p0 += C::C_COLS) {
-                if (lane == 0) {
-                    // the pass's residual slice; the first one is in flight while the MMAs run
-                    bulk_wait_read0();   // the previous store has finished reading sw
-                    mbar_expect_tx(&cfull[q], C::C_WARP_BYTES);
-#pragma unroll
-                    for (int j = 0; j < NB; ++j)
-                        tma_load_2d(sw + j * 4096, &tma_c, &cfull[q], n0 + p0 + j * 32, m0);
-                }
-                if (p0 == 0) {
-                    mbar_wait(&tfull[acc], acc_phase);
-                    tc_fence_after();
-                    if (q == 2 && lane == 0) RF_TRACE(it, 4);
-                }
+            for (int p = 0; p < NP; ++p) {
                 mbar_wait(&cfull[q], c_phase);
                 c_phase ^= 1;
 #pragma unroll 1
                 for (int j = 0; j < NB; ++j) {
+                    const int col = p * CC + j * 32;
                     uint32_t r[32];
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + p0 + j * 32), r);
-                    float4 gv[8];
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) gv[v] = __ldg((const float4 *)(g + p0 + j * 32 + v * 4));
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col), r);
                     tmem_ld_wait();
                     float4 *row = (float4 *)(sw + j * 4096 + lane * 128);
+                    const float4 *gv = (const float4 *)(gr + col);
 #pragma unroll
                     for (int v = 0; v < 8; ++v) {
+                        const float4 g4 = gv[v];
                         float4 x = row[v ^ (lane & 7)];
-                        x.x += gv[v].x * __uint_as_float(r[4 * v]);
-                        x.y += gv[v].y * __uint_as_float(r[4 * v + 1]);
-                        x.z += gv[v].z * __uint_as_float(r[4 * v + 2]);
-                        x.w += gv[v].w * __uint_as_float(r[4 * v + 3]);
+                        x.x += g4.x * __uint_as_float(r[4 * v]);
+                        x.y += g4.y * __uint_as_float(r[4 * v + 1]);
+                        x.z += g4.z * __uint_as_float(r[4 * v + 2]);
+                        x.w += g4.w * __uint_as_float(r[4 * v + 3]);
                         row[v ^ (lane & 7)] = x;
                     }
                 }
+                if (p == NP - 1) tc_fence_before();
                 fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
                 __syncwarp();
                 if (lane == 0) {
+                    if (p == NP - 1) {   // the accumulator has been read: release it
+                        if constexpr (CG == 2)
+                            mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+                        else
+                            mbar_arrive(&tempty[acc]);
+                    }
 #pragma unroll
-                    for (int j = 0; j < NB; ++j) tma_store_2d(&tma_c, sw + j * 4096, n0 + p0 + j * 32, m0);
+                    for (int j = 0; j < NB; ++j) tma_store_2d(&tma_c, sw + j * 4096, n0 + p * CC + j * 32, m0);
                     bulk_commit();
+                    if (p == NP - 1 && q == 2) RF_TRACE(it, 5);
+                    const bool more = p + 1 < NP || t + units < num_tiles;
+                    if (more) {
+                        bulk_wait_read0();   // the store has read the slice: the buffer is free
+                        if (p + 1 < NP)
+                            load_pass(t, p + 1);
+                        else
+                            load_pass(t + units, 0);
+                    }
                 }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (q == 2) RF_TRACE(it, 5);
-                if constexpr (CG == 2)
-                    mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
-                else
-                    mbar_arrive(&tempty[acc]);
             }
             if (++acc == 2) {
                 acc = 0;
@@ -431,6 +464,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         __syncthreads();
         if (warp == 1) tmem_dealloc<2 * BN>(tmem);
     }
+    RF_GTRACE(14);
 }
 
 }  // namespace rf::gemm

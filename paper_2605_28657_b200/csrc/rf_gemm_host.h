@@ -39,7 +39,7 @@ int gemm_run(const GemmPlan &p, int epi, void *out, int64_t ldo, const float *ga
 
 // tcgen05 attention (rf_attention_tc.cu): tensor maps over Q, K and V^T built once.
 struct AttnPlan {
-    CUtensorMap tq, tk, tvt;
+    CUtensorMap tq, tk, tvt, tk64;   // tk64: 64-key boxes (rf_attn_fa64_kernel)
     int B, Nq, Nk, Nk_pad, H, Hkv;
 };
 int attn_plan(AttnPlan *p, const void *q, int64_t ldq_elems, int64_t q_cols, const void *k, int64_t ldk_elems,

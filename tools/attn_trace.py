@@ -22,7 +22,7 @@ def main():
     vt = torch.randn(B, Hk, 128, pad, device="cuda").bfloat16()
     out = torch.empty(B * Nq, H * 128, device="cuda", dtype=torch.bfloat16)
     nq, ncta = (Nq + 127) // 128, (Nq + 127) // 128 * B * H // 2
-    buf = torch.zeros(ncta * 8 * 16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(ncta * 16 * 16, dtype=torch.int64, device="cuda")
 
     def run():
         _native.check(lib.rf_attention_tc_bf16(vp(q.data_ptr()), vp(k.data_ptr()), vp(vt.data_ptr()),
@@ -36,7 +36,7 @@ def main():
     run()
     torch.cuda.synchronize()
     lib.rf_attn_set_trace(vp(0))
-    t = buf.cpu().numpy().reshape(ncta, 8, 16).astype(np.float64)
+    t = buf.cpu().numpy().reshape(ncta, 16, 16).astype(np.float64)
     nt = (Nk + 127) // 128
     for c in (0, 1, ncta // 2):
         t0 = t[c, 4, 0]
@@ -54,6 +54,10 @@ def main():
     g0, g1 = t[:, 0, 15], t[:, 1, 15]
     print(f"kernel span {(g1.max() - g0.min()) / 1e3:.1f} us; CTA durations median {np.median(g1 - g0) / 1e3:.1f} us "
           f"max {np.max(g1 - g0) / 1e3:.1f}; start offsets: {np.percentile(g0 - g0.min(), [0, 50, 75, 90, 100]) / 1e3}")
+    for name, a, b in (("wait->S loaded", 4, 8), ("S loaded->max done", 8, 10), ("exps+stores issued", 10, 12),
+                       ("st_wait+arrive", 12, 6)):
+        d = np.concatenate([(t[:, b + h, :nt - 1] - t[:, a + h, :nt - 1]).ravel() for h in range(2)])
+        print(f"  {name:22s} median {np.median(d):6.0f} cyc")
     print(f"median softmax per head-tile {np.median(soft):.0f} cyc; S issue->ready {np.median(lat):.0f}; "
           f"PV issue->S issue {np.median(gap):.0f}; CTA span {np.median(t[:, 6:8, nt - 1].max(1) - t[:, 4, 0]):.0f}")
 

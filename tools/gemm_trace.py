@@ -43,6 +43,10 @@ def trace(M, N, K, epi, bn, pair, label):
                 epis.append(t[c, i, 5] - t[c, i, 4])      # epilogue (warp 2)
     span = [t[c, :, 5].max() - t[c, 0, 0] for c in leaders]
     f = lambda v: f"{np.median(v):8.0f} (max {np.max(v):8.0f})" if len(v) else "-"
+    ent, post, ext = t[:, 15, 7], t[:, 13, 7], t[:, 14, 7]
+    print(f"{label}: globaltimer kernel span {(ext.max() - ent.min()) / 1e3:.1f} us; entry spread "
+          f"{(ent.max() - ent.min()) / 1e3:.1f} us; entry->after pdl/prologue median {np.median(post - ent) / 1e3:.2f} us; "
+          f"CTA duration median {np.median(ext - ent) / 1e3:.1f} us; cycles/us {np.median(span) / max(1e-9, np.median(ext - post) / 1e3):.0f}")
     print(f"{label}: tiles/unit {min(ntiles)}-{max(ntiles)} | mainloop cyc {f(mains)} | acc-wait {f(waits)} | "
           f"stage-lead {f(leads)} | epilogue {f(epis)} | span {f(span)}", flush=True)
 
