@@ -314,7 +314,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
     return make_float2(__uint_as_float(r0), __uint_as_float(r1));
 }
 
-constexpr int kPolyPairs = 6;   // of 16 exponential pairs per 32-column chunk (see exp2_poly2)
+constexpr int kPolyPairs = 0;   // of 16 exponential pairs per 32-column chunk (see exp2_poly2)
 
 // NH = 2: three full warpgroups (two softmax groups + one with the MMA and TMA warps) so
 // registers can be moved between them with setmaxnreg; NH = 1: softmax group + 2 warps.
@@ -334,13 +334,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 #define FA_GTRACE(ev)                                                                                     \
     do {                                                                                                  \
-        if (g_attn_trace)                                                                                 \
-            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)) * 16 + 15] = globaltimer(); \
+        if (trace_buf)                                                                                    \
+            trace_buf[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)) * 16 + 15] = globaltimer(); \
     } while (0)
 #define FA_TRACE(ev, j)                                                                                  \
     do {                                                                                                 \
-        if (g_attn_trace && (j) < 16)                                                                    \
-            g_attn_trace[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)) * 16 + (j)] = clock64(); \
+        if (trace_buf && (j) < 16)                                                                       \
+            trace_buf[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)) * 16 + (j)] = clock64(); \
     } while (0)
 
 // KVS = K/V stages: 2 (double-buffered) or 1 (one key tile, e.g. the cross-attention: the
@@ -352,6 +352,7 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
                   const __grid_constant__ CUtensorMap tvt, __nv_bfloat16 *__restrict__ out, int64_t ldo, int Nq,
                   int Nk, int H, int Hkv, float scale_log2) {
     extern __shared__ uint8_t smem_raw[];
+    unsigned long long *const trace_buf = g_attn_trace;   // debugging timeline (null in production)
     uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = base;                 // [NH]
     uint8_t *sK = sQ + NH * kOperand;     // [KVS]
@@ -594,9 +595,11 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 // Self-attention over 64-key tiles with double-buffered scores (the default when the GQA
 // head pair shares a KV head and there is more than one 128-key tile).
 //
-// CTA = one 128-row query tile x the 2 query heads of one KV head; 12 warps: warpgroup a
-// (a = 0, 1) runs head a's softmax (one query row per thread), warp 8 issues the MMAs,
-// warp 9 the TMA loads.  Per head, S_j = Q K_j^T (M=128, N=64) goes into one of two
+// CTA = one 128-row query tile x NH query heads of one KV head: warpgroup a runs head a's
+// softmax (one query row per thread), warp 4 NH issues the MMAs, warp 4 NH + 1 the TMA
+// loads.  NH = 1 fits two CTAs per SM (96 KB shared memory, 256 TMEM columns): the two
+// CTAs' softmax and MMA phases interleave, and 384 head tiles balance over 296 slots
+// better than 192 head-pair tiles over 148.  Per head, S_j = Q K_j^T (M=128, N=64) goes into one of two
 // 64-column TMEM buffers, so S_{j+1} is computed while the softmax works on S_j: the
 // tensor core never waits for the softmax and the softmax never waits for a fresh S.
 // P_j (bf16) overwrites the first 32 columns of its S buffer and O += P_j V_j reads it
@@ -604,36 +607,42 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 // ... PV(j-1), S(j+1), PV(j), S(j+2) ... -- tcgen05 executes in issue order, so S(j+2)
 // cannot overwrite P(j) before PV(j) has read it.  Running max with lazy O rescaling
 // (only when the tile max grows by more than 2^8; the softmax first waits for PV(j-1)).
-// TMEM: head a: S buffers at columns a*128 + {0, 64}, O at 256 + a*128 (512 total).
-// K / V^T tiles: KS-stage rings of 16 KB each.
+// TMEM: head a: S buffers at columns a*128 + {0, 64}, O at NH*128 + a*128.
+// K / V^T tiles: KS-stage rings of 16 KB each (KS = 4 for NH = 2, 2 for NH = 1).
 constexpr int kKeys64 = 64;
-constexpr int kFa64Stages = 4;
+template <int NH>
+constexpr int fa64_stages() { return NH == 2 ? 4 : 2; }
 constexpr uint32_t kK64Half = 64 * 64 * 2;        // [64 keys][64 dims] bf16, SW128
 constexpr uint32_t kK64Tile = 2 * kK64Half;       // [64 keys][128 dims]
 constexpr uint32_t kV64Tile = 128 * 64 * 2;       // [128 dims][64 keys]
-constexpr size_t fa64_smem() { return 1024 + 2 * (size_t)kOperand + kFa64Stages * (size_t)(kK64Tile + kV64Tile) + 256; }
+template <int NH>
+constexpr size_t fa64_smem() {
+    return 1024 + NH * (size_t)kOperand + fa64_stages<NH>() * (size_t)(kK64Tile + kV64Tile) + 256;
+}
 
-template <int PE>
-__global__ void __launch_bounds__(384, 1)
+template <int NH, int PE>
+__global__ void __launch_bounds__(128 * NH + 64, NH == 1 ? 2 : 1)
 rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tvt, __nv_bfloat16 *__restrict__ out, int64_t ldo, int Nq,
                     int Nk, int H, int Hkv, float scale_log2) {
-    constexpr int KS = kFa64Stages;
+    constexpr int KS = fa64_stages<NH>();
     extern __shared__ uint8_t smem_raw[];
+    unsigned long long *const trace_buf = g_attn_trace;   // debugging timeline (null in production)
     uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *sQ = base;                    // [2 heads] x 32 KB
-    uint8_t *sK = sQ + 2 * kOperand;       // [KS] x 16 KB
+    uint8_t *sQ = base;                    // [NH heads] x 32 KB
+    uint8_t *sK = sQ + NH * kOperand;      // [KS] x 16 KB
     uint8_t *sV = sK + KS * kK64Tile;      // [KS] x 16 KB (V^T: rows = head dims)
     uint64_t *bar = (uint64_t *)(sV + KS * kV64Tile);
     uint64_t *qfull = bar, *kfull = bar + 1, *kempty = kfull + KS, *vfull = kempty + KS, *vempty = vfull + KS;
     uint64_t *sfull = vempty + KS;         // [head * 2 + buffer]
-    uint64_t *pfull = sfull + 4, *odone = pfull + 2;
-    uint32_t *tmem_slot = (uint32_t *)(odone + 2);
+    uint64_t *pfull = sfull + 2 * NH, *odone = pfull + NH;
+    uint32_t *tmem_slot = (uint32_t *)(odone + NH);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int MMA_WARP = 8, TMA_WARP = 9;
+    constexpr int MMA_WARP = 4 * NH, TMA_WARP = 4 * NH + 1;
+    constexpr uint32_t TO = NH * 128;      // O column base in TMEM
     const int group = H / Hkv;
-    const int bh = blockIdx.y, per_b = H / 2, b = bh / per_b, h0 = (bh % per_b) * 2;
+    const int bh = blockIdx.y, per_b = H / NH, b = bh / per_b, h0 = (bh % per_b) * NH;
     const int hk = h0 / group;
     const int q0 = blockIdx.x * kTcRows;
     const int nt = (Nk + kKeys64 - 1) / kKeys64;
@@ -650,14 +659,14 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             mbar_init(&vfull[i], 1);
             mbar_init(&vempty[i], 1);
         }
-        for (int i = 0; i < 4; ++i) mbar_init(&sfull[i], 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 2 * NH; ++i) mbar_init(&sfull[i], 1);
+        for (int i = 0; i < NH; ++i) {
             mbar_init(&pfull[i], 4);   // the 4 softmax warps of the head
             mbar_init(&odone[i], 1);
         }
         mbar_fence_init();
     }
-    if (warp == MMA_WARP) tmem_alloc<512>(tmem_slot);
+    if (warp == MMA_WARP) tmem_alloc<256 * NH>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -668,8 +677,8 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
 
     if (warp == TMA_WARP) {
         if (elect_one()) {
-            mbar_expect_tx(qfull, 2 * kOperand);
-            for (int a = 0; a < 2; ++a) {
+            mbar_expect_tx(qfull, NH * kOperand);
+            for (int a = 0; a < NH; ++a) {
                 tma_load_2d(sQ + a * kOperand, &tq, qfull, (h0 + a) * 128, b * Nq + q0);
                 tma_load_2d(sQ + a * kOperand + kTile, &tq, qfull, (h0 + a) * 128 + 64, b * Nq + q0);
             }
@@ -677,10 +686,12 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
                 const int s = j % KS;
                 const uint32_t ph = ((j / KS) & 1) ^ 1;
                 mbar_wait(&kempty[s], ph);
+                FA_TRACE(13, j);
                 mbar_expect_tx(&kfull[s], kK64Tile);
                 tma_load_2d(sK + s * kK64Tile, &tk, &kfull[s], hk * 128, b * Nk + j * kKeys64);
                 tma_load_2d(sK + s * kK64Tile + kK64Half, &tk, &kfull[s], hk * 128 + 64, b * Nk + j * kKeys64);
                 mbar_wait(&vempty[s], ph);
+                FA_TRACE(14, j);
                 mbar_expect_tx(&vfull[s], kV64Tile);
                 tma_load_2d(sV + s * kV64Tile, &tvt, &vfull[s], j * kKeys64, (b * Hkv + hk) * 128);
             }
@@ -700,7 +711,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const uint64_t bd = sdesc_sw128(sV + s * kV64Tile) + (uint64_t)(ks * 2);
-                    umma_bf16_ts(tmem + 256 + a * 128, tmem + a * 128 + buf * 64 + ks * 8, bd, idesc_o,
+                    umma_bf16_ts(tmem + TO + a * 128, tmem + a * 128 + buf * 64 + ks * 8, bd, idesc_o,
                                  (acc || ks > 0) ? 1u : 0u);
                 }
                 umma_commit(&odone[a]);
@@ -709,26 +720,27 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             for (int j = 0; j < 2 && j < nt; ++j) {
                 mbar_wait(&kfull[j], 0);
                 tc_fence_after();
-                mma_s(0, j, j);
-                mma_s(1, j, j);
+                FA_TRACE(2, j);
+#pragma unroll
+                for (int a = 0; a < NH; ++a) mma_s(a, j, j);
                 umma_commit(&kempty[j]);
             }
             for (int j = 0; j < nt; ++j) {
                 const int s = j % KS, s2 = (j + 2) % KS, buf = j & 1;
 #pragma unroll 1
-                for (int a = 0; a < 2; ++a) {
+                for (int a = 0; a < NH; ++a) {
                     mbar_wait(&pfull[a], j & 1);
                     if (a == 0) mbar_wait(&vfull[s], (j / KS) & 1);
                     tc_fence_after();
                     FA_TRACE(a, j);
                     mma_o(a, s, buf, j > 0);
-                    if (a == 1) umma_commit(&vempty[s]);
+                    if (a == NH - 1) umma_commit(&vempty[s]);
                     if (j + 2 < nt) {
                         if (a == 0) mbar_wait(&kfull[s2], ((j + 2) / KS) & 1);
                         tc_fence_after();
                         FA_TRACE(2 + a, j + 2);
                         mma_s(a, s2, buf);
-                        if (a == 1) umma_commit(&kempty[s2]);
+                        if (a == NH - 1) umma_commit(&kempty[s2]);
                     }
                 }
             }
@@ -736,7 +748,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
     } else if (warp < MMA_WARP) {
         const int a = warp >> 2, quarter = warp & 3;
         const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-        const uint32_t tO = tmem + lane_base + 256 + a * 128;
+        const uint32_t tO = tmem + lane_base + TO + a * 128;
         float m = 0.f, l = 0.f;
         for (int j = 0; j < nt; ++j) {
             const int buf = j & 1;
@@ -748,6 +760,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             tmem_ld32(tS, *(uint32_t(*)[32])(r));
             tmem_ld32(tS + 32, *(uint32_t(*)[32])(r + 32));
             tmem_ld_wait();
+            if (quarter == 0 && lane == 0) FA_TRACE(8 + a, j);
             const int valid = Nk - j * kKeys64;
             if (valid < kKeys64) {   // the last key tile: keys >= valid are masked
 #pragma unroll
@@ -766,6 +779,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
                 m = tmax;
             } else {
                 mbar_wait(&odone[a], (j - 1) & 1);   // PV(j-1) done: O stable (and phases tracked exactly)
+                if (quarter == 0 && lane == 0) FA_TRACE(10 + a, j);
                 const bool need = tmax > m + 8.f;
                 if (__any_sync(0xffffffffu, need)) {   // lazy rescale of O and l
                     tc_fence_after();
@@ -803,6 +817,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
                 l += __uint_as_float((uint32_t)ls) + __uint_as_float((uint32_t)(ls >> 32));
                 tmem_st16(tS + c * 16, pk);
             }
+            if (quarter == 0 && lane == 0) FA_TRACE(12 + a, j);
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -838,7 +853,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
     tc_fence_before();
     __syncthreads();
     if (tid == 0) FA_GTRACE(1);
-    if (warp == MMA_WARP) tmem_dealloc<512>(tmem);
+    if (warp == MMA_WARP) tmem_dealloc<256 * NH>(tmem);
 }
 
 int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const void *k, int64_t ldk, int64_t k_cols,
@@ -883,27 +898,35 @@ static int launch_fa_pe(const AttnPlan &p, void *out, int64_t ldo, int B, float 
     return launch_fa_pp<NH, KVS, PE, false>(p, out, ldo, B, sc, st);
 }
 
-static int poly_pairs() {   // RF_ATTN_POLY overrides the share of FMA-pipe exponentials (tuning aid)
-    static const int v = [] {
-        const char *e = getenv("RF_ATTN_POLY");
-        return e ? atoi(e) : kPolyPairs;
-    }();
-    return v;
+// Tuning aids (not product ABI): RF_ATTN_POLY / RF_ATTN_FA64 at first use, or rf_attn_set_variant.
+static int g_poly = -1, g_fa64 = -1;
+static int poly_pairs() {   // exponential pairs (of 16) computed on the FMA pipe
+    if (g_poly < 0) g_poly = getenv("RF_ATTN_POLY") ? atoi(getenv("RF_ATTN_POLY")) : kPolyPairs;
+    return g_poly;
 }
 
-template <int PE>
+template <int NH, int PE>
 static int launch_fa64(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa64_kernel<PE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)fa64_smem()));
+        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa64_kernel<NH, PE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fa64_smem<NH>()));
         attr = true;
     }
-    dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / 2);
-    RF_TRY_CUDA(launch_pdl(rf_attn_fa64_kernel<PE>, grid, dim3(384), fa64_smem(), st, p.tq, p.tk64, p.tvt,
-                           (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
+    dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / NH);
+    RF_TRY_CUDA(launch_pdl(rf_attn_fa64_kernel<NH, PE>, grid, dim3(128 * NH + 64), fa64_smem<NH>(), st, p.tq,
+                           p.tk64, p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
     RF_TRY_LAUNCH("rf_attn_fa64_kernel");
     return RF_OK;
+}
+
+template <int NH>
+static int launch_fa64_pe(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+    switch (poly_pairs()) {
+        case 0: return launch_fa64<NH, 0>(p, out, ldo, B, sc, st);
+        case 4: return launch_fa64<NH, 4>(p, out, ldo, B, sc, st);
+        default: return launch_fa64<NH, 6>(p, out, ldo, B, sc, st);
+    }
 }
 
 template <int NH, int KVS>
@@ -925,14 +948,14 @@ int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) 
         // one key tile (cross-attention to 128 conditioning tokens): one head per CTA, two CTAs
         // per SM; longer key ranges: the GQA head pair ping-pongs inside one CTA
         if (p.Nk <= kTcRows) return launch_fa<1, 1>(p, out, ldo, B, sc, st);
-        static const int fa64 = getenv("RF_ATTN_FA64") ? atoi(getenv("RF_ATTN_FA64")) : 1;
-        if (pair && fa64) {
-            switch (poly_pairs()) {
-                case 0: return launch_fa64<0>(p, out, ldo, B, sc, st);
-                case 4: return launch_fa64<4>(p, out, ldo, B, sc, st);
-                default: return launch_fa64<6>(p, out, ldo, B, sc, st);
-            }
-        }
+        // RF_ATTN_FA64 (tuning aid): 1 = 64-key kernel, one head per CTA (default); 2 = 64-key
+        // kernel, GQA head pair per CTA; 0 = the 128-key head-pair ping-pong kernel
+        if (g_fa64 < 0) g_fa64 = getenv("RF_ATTN_FA64") ? atoi(getenv("RF_ATTN_FA64")) : 1;
+        const int fa64 = g_fa64;
+        if (fa64 == 2 && pair) return launch_fa64_pe<2>(p, out, ldo, B, sc, st);
+        if (fa64 == 1) return launch_fa64_pe<1>(p, out, ldo, B, sc, st);
+        if (fa64 == 3) return launch_fa<1, 1>(p, out, ldo, B, sc, st);   // 128-key tiles, 2 CTAs / SM
+        if (fa64 == 4) return launch_fa<1, 2>(p, out, ldo, B, sc, st);
         return pair ? launch_fa<2, 2>(p, out, ldo, B, sc, st) : launch_fa<1, 2>(p, out, ldo, B, sc, st);
     }
     if (pair) {
@@ -969,6 +992,11 @@ using namespace rf;
 extern "C" int rf_attn_set_trace(void *buf) {
     unsigned long long *p = (unsigned long long *)buf;
     return cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)) == cudaSuccess ? RF_OK : RF_ECUDA;
+}
+
+extern "C" void rf_attn_set_variant(int fa64, int poly) {
+    g_fa64 = fa64;
+    g_poly = poly;
 }
 
 extern "C" int rf_attention_tc_bf16(const void *q, const void *k, const void *vt, void *out, int32_t batch,

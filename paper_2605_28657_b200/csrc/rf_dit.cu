@@ -394,6 +394,10 @@ static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shi
 // The forward body: a fixed launch sequence for a given row count and output buffer
 // (every per-call input is read from d.rows_dev), so it can be captured into a graph.
 static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
+    // RF_DIT_SKIP (timing ablation only; the output is garbage): bit mask of per-layer kernel
+    // classes left out -- 1 norms, 2 self-attention, 4 cross-attention, 8 QKV, 16 O, 32 cross-Q,
+    // 64 cross-O, 128 gate-up, 256 down (tools/dit_ablate.py)
+    static const int skip = getenv("RF_DIT_SKIP") ? atoi(getenv("RF_DIT_SKIP")) : 0;
     const rf_dit_config &c = d.c;
     const int64_t N = d.tokens, M = (int64_t)rows * N, D = c.d_model, L = c.n_layers, B = rows;
     const int64_t W6 = 6 * D, Nc = c.n_cond_tokens;
@@ -426,30 +430,32 @@ static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
     for (int64_t l = 0; l < L; ++l) {
         const float *md = d.mods + l * B * W6;  // [B][6][D]: shift,scale,gate (msa), shift,scale,gate (mlp)
         // self-attention
-        RF_TRY(norm_mod(d, d.h, M, md + 0 * D, md + 1 * D, W6, d.a, st));
+        if (!(skip & 1)) RF_TRY(norm_mod(d, d.h, M, md + 0 * D, md + 1 * D, W6, d.a, st));
         const VtOut vts{d.vt_self, (int)(d.q_dim + d.kv_dim), c.n_kv_heads, d.n_pad};
-        RF_TRY(gemm_run(d.p_qkv[l], 5 /* bf16 + RoPE */, d.qkv, d.qkv_dim, nullptr, 0, (int)N, 1.f, st, d.rope,
+        if (!(skip & 8)) RF_TRY(gemm_run(d.p_qkv[l], 5 /* bf16 + RoPE */, d.qkv, d.qkv_dim, nullptr, 0, (int)N, 1.f, st, d.rope,
                         (int)(d.q_dim + d.kv_dim), M, d.tc_attention ? &vts : nullptr));
-        if (d.tc_attention)
+        if (skip & 2) {
+        } else if (d.tc_attention)
             RF_TRY(attn_run(d.a_self, d.att, d.q_dim, (int)B, st));
         else
             RF_TRY(rf_attention_bf16(d.qkv, d.qkv + d.q_dim, d.qkv + d.q_dim + d.kv_dim, d.att, (int)B, (int)N,
                                      (int)N, c.n_heads, c.n_kv_heads, d.qkv_dim, d.qkv_dim, d.qkv_dim, d.q_dim, st));
-        RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
+        if (!(skip & 16)) RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
         // cross-attention to the row's conditioning tokens (residual, no gate)
-        RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
-        RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+        if (!(skip & 1)) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
+        if (!(skip & 32)) RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
         const __nv_bfloat16 *kvl = d.kvc + l * 2 * d.kv_dim;
-        if (d.tc_attention)
+        if (skip & 4) {
+        } else if (d.tc_attention)
             RF_TRY(attn_run(d.a_cross[l], d.att, d.q_dim, (int)B, st));
         else
             RF_TRY(rf_attention_bf16(d.qc, kvl, kvl + d.kv_dim, d.att, (int)B, (int)N, (int)Nc, c.n_heads,
                                      c.n_kv_heads, d.q_dim, L * 2 * d.kv_dim, L * 2 * d.kv_dim, d.q_dim, st));
-        RF_TRY(gemm_run(d.p_oc[l], RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));
+        if (!(skip & 64)) RF_TRY(gemm_run(d.p_oc[l], RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));
         // SwiGLU MLP
-        RF_TRY(norm_mod(d, d.h, M, md + 3 * D, md + 4 * D, W6, d.a, st));
-        RF_TRY(gemm_run(d.p_gu[l], RF_EPI_SWIGLU, d.mlp, c.mlp_hidden, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
-        RF_TRY(gemm_run(d.p_down[l], RF_EPI_RESID_GATE, d.h, D, md + 5 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
+        if (!(skip & 1)) RF_TRY(norm_mod(d, d.h, M, md + 3 * D, md + 4 * D, W6, d.a, st));
+        if (!(skip & 128)) RF_TRY(gemm_run(d.p_gu[l], RF_EPI_SWIGLU, d.mlp, c.mlp_hidden, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+        if (!(skip & 256)) RF_TRY(gemm_run(d.p_down[l], RF_EPI_RESID_GATE, d.h, D, md + 5 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
     }
     // final AdaLN + output projection (fp32), tokens [B, N, p*C] == latent [B, T, C]
     RF_TRY(norm_mod(d, d.h, M, d.fmod, d.fmod + D, 2 * D, d.a, st));

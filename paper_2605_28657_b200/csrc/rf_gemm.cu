@@ -76,7 +76,7 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait()
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
     at[1].id = cudaLaunchAttributeClusterDimension;
     at[1].val.clusterDim.x = CG;
     at[1].val.clusterDim.y = 1;

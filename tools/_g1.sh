@@ -1,5 +1,7 @@
-O=gpurun_out/r1j; mkdir -p $O
-timeout 120 python tools/gemm_trace.py > $O/gemm_trace.txt 2>&1
-timeout 300 python -m pytest tests -m gpu -q -x -k "gemm or dit" > $O/pytest.txt 2>&1
-timeout 120 python tools/dit_check.py 4 --graph > $O/dit_check.txt 2>&1
-grep resid $O/gemm_trace.txt; tail -2 $O/pytest.txt; cat $O/dit_check.txt
+O=gpurun_out/r1u; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
+tail -n 3 $O/pytest_gpu.log $O/smoke.log; python -c "
+import json; d=json.load(open('$O/bench.json')); print(d['value'], d['ms_per_step'], d['phase_ms'], d['roofline']['frac'], d['e2e']['value'], d['clocks'])"
+tail -n 3 $O/bench.err

@@ -21,7 +21,7 @@ def main():
     pad = (Nk + 7) // 8 * 8
     vt = torch.randn(B, Hk, 128, pad, device="cuda").bfloat16()
     out = torch.empty(B * Nq, H * 128, device="cuda", dtype=torch.bfloat16)
-    nq, ncta = (Nq + 127) // 128, (Nq + 127) // 128 * B * H // 2
+    nq, ncta = (Nq + 127) // 128, (Nq + 127) // 128 * B * H // (1 if os.environ.get("RF_ATTN_FA64", "1") == "1" else 2)
     buf = torch.zeros(ncta * 16 * 16, dtype=torch.int64, device="cuda")
 
     def run():
