@@ -258,21 +258,29 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     curve = np.linspace(0.0, 1.0, T)
+    codec = rf.ToyCodec(channels=D, hop=HOP)
+    gate = rf.GatedDecoder(codec, window_frames=WINDOW, overlap=OVERLAP)
     t0 = time.perf_counter()
     e2e_done, h2d, d2h = 0, 0, 0
     for k in range(args.steps):
-        pipe.set_shared_curve("sde_denoise_curve", curve if k % 2 else 1.0)   # host -> device, [T] f64
+        # a control write every tick whose value flips every 8 ticks, so the similarity filter
+        # sees both settled and changing completions
+        pipe.set_shared_curve("sde_denoise_curve", curve if (k // 8) % 2 else 1.0)   # host -> device, [T] f64
         h2d += T * 8
         for r in pipe.tick():
             _ = r.latent                                                       # device -> host, [T, D] f64
             d2h += T * D * 8
+            gate.feed(r)                                                       # gated 3-s window decode
+            d2h += gate.latest_pcm().samples.nbytes                            # device -> host, int16 PCM
             e2e_done += 1
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    gated = {"window_frames": WINDOW, "overlap": OVERLAP, "decodes": gate.decodes, "skips": gate.skips,
+             "skip_rate": round(gate.skip_rate, 3),
+             "note": "similarity-filter-gated decode (PAPER.md:203): flagged completions reuse the last chunk"}
     pipe.set_shared_curve("sde_denoise_curve", 1.0)
 
     # ---- windowed decode (3-s window + overlap 15) of the last completion ----
-    codec = rf.ToyCodec(channels=D, hop=HOP)
     lat = pipe._last_emitted
     with torch.cuda.stream(st):
         for _ in range(3):
@@ -340,8 +348,10 @@ def run_ours(args):
                    "completions_timed": int(completions_all)},
         "e2e": {"value": round(e2e_all / e2e_max, 3), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
-                "note": "wall clock through StreamPipeline: per-tick shared-curve write from host, "
-                        "CompletionRecord.latent read back to host"},
+                "note": "wall clock through StreamPipeline: a host shared-curve write every tick (value flips every 8), "
+                        "every CompletionRecord.latent read back to host, its 3-s playback window decoded "
+                        "through GatedDecoder and the int16 PCM read back to host",
+                "gated_decode": gated},
         "windowed_decode_ms": round(decode_ms, 5),
         "decode_240s": long_decode,
         "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
