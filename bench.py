@@ -133,6 +133,16 @@ def make_request(rf, stream_id):
     return rf.GenerationRequest(conditions=(cond,))
 
 
+def forward_traffic():
+    """DRAM bytes of one DiT forward from the committed ncu launch list (tools/forward_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_dit_forward_traffic.json")) as fh:
+            t = json.load(fh)
+        return t["warm"]["dram_bytes"], t["cold"]["dram_bytes"]
+    except Exception:
+        return None, None
+
+
 def solve_bytes_per_row(toy: bool):
     # rf_tick_kernel, per element: x read + write (f64), source (f64), sde noise (f64);
     # toy model adds the x0 table, the style offset and the model noise (f64);
@@ -357,7 +367,10 @@ def run_ours(args):
         "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
         "roofline": {"bound": "tensor", "kernel": "dit_forward (tcgen05 GEMMs + attention + norms, one launch set)",
                      "achieved": round(dit_tflops, 1), "peak": bf16_sust, "unit": "TFLOP/s",
-                     "frac": round(dit_tflops / bf16_sust, 4), "traffic": None,
+                     "frac": round(dit_tflops / bf16_sust, 4), "traffic": forward_traffic()[0],
+                     "traffic_note": "DRAM read+write bytes of one forward (sum over its 279 launches) from the "
+                                     "committed ncu launch list profiles/r1_dit_forward_traffic.json, "
+                                     f"--cache-control none; cold-cache sum {forward_traffic()[1]}",
                      "algorithmic_flops_per_launch": dit_flops,
                      "peak_source": f"{peak_src} bf16 sustained (burst {bf16_burst})"},
         "gpu_launches": int(launches),

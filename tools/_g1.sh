@@ -1,7 +1,6 @@
-O=gpurun_out/r1u; mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
-timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
-tail -n 3 $O/pytest_gpu.log $O/smoke.log; python -c "
-import json; d=json.load(open('$O/bench.json')); print(d['value'], d['ms_per_step'], d['phase_ms'], d['roofline']['frac'], d['e2e']['value'], d['clocks'])"
-tail -n 3 $O/bench.err
+O=gpurun_out/r1w; mkdir -p $O
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+timeout 900 ncu --metrics $M --clock-control none -c 700 --csv --log-file $O/fw_cold.csv python tools/dit_check.py 4 --no-ref > $O/ncu_cold.log 2>&1
+timeout 900 ncu --metrics $M --clock-control none --cache-control none -c 700 --csv --log-file $O/fw_warm.csv python tools/dit_check.py 4 --no-ref > $O/ncu_warm.log 2>&1
+python tools/forward_traffic.py $O/fw_cold.csv $O/fw_warm.csv $O/forward_traffic.json
+python tools/launches.py $O/fw_warm.csv | head -20
