@@ -80,6 +80,45 @@ def test_tcgen05_attention_vs_sdpa(dit_mod, B, Nq, Nk, H, Hk, grow):
     assert rel_rms(out, ref) < 1e-2
 
 
+@pytest.mark.parametrize("variant", [(0, 0), (0, 4), (1, 4), (1, 6), (2, 0), (2, 4), (3, 0), (4, 0)])
+@pytest.mark.parametrize("B,Nq,Nk,H,Hk,grow", [(2, 750, 750, 16, 8, 1), (1, 200, 333, 4, 2, 0)])
+def test_attention_variants_vs_sdpa(dit_mod, variant, B, Nq, Nk, H, Hk, grow):
+    """Every self-attention kernel variant (rf_attn_set_variant: 64-key one-head / head-pair,
+    128-key ping-pong / two-CTA, exponentials partly on the FMA pipe) against SDPA."""
+    import ctypes
+
+    from paper_2605_28657_b200 import _native
+
+    lib = _native.load()
+    lib.rf_attention_tc_bf16.restype = int
+    g = torch.Generator(device="cuda").manual_seed(Nq * 13 + Nk)
+    q = torch.randn(B * Nq, H * 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B * Nk, Hk * 128, device="cuda", generator=g)
+    if grow:
+        k = k * torch.linspace(0.3, 4.0, Nk, device="cuda").repeat(B)[:, None]
+    k = k.bfloat16()
+    v = torch.randn(B * Nk, Hk * 128, device="cuda", generator=g).bfloat16()
+    nk_pad = (Nk + 7) // 8 * 8
+    vt = torch.zeros(B, Hk, 128, nk_pad, device="cuda", dtype=torch.bfloat16)
+    vt[..., :Nk] = v.reshape(B, Nk, Hk, 128).permute(0, 2, 3, 1)
+    out = torch.empty(B * Nq, H * 128, device="cuda", dtype=torch.bfloat16)
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    lib.rf_attn_set_variant(*variant)
+    try:
+        _native.check(lib.rf_attention_tc_bf16(vp(q.data_ptr()), vp(k.data_ptr()), vp(vt.data_ptr()),
+                                               vp(out.data_ptr()), B, Nq, Nk, nk_pad, H, Hk, i64(H * 128),
+                                               i64(Hk * 128), i64(H * 128),
+                                               vp(torch.cuda.current_stream().cuda_stream)), "attn")
+        torch.cuda.synchronize()
+    finally:
+        lib.rf_attn_set_variant(-1, -1)   # back to the defaults
+    qq = q.float().reshape(B, Nq, H, 128).transpose(1, 2)
+    kk = k.float().reshape(B, Nk, Hk, 128).repeat_interleave(H // Hk, 2).transpose(1, 2)
+    vv = v.float().reshape(B, Nk, Hk, 128).repeat_interleave(H // Hk, 2).transpose(1, 2)
+    ref = torch.nn.functional.scaled_dot_product_attention(qq, kk, vv).transpose(1, 2).reshape(B * Nq, H * 128)
+    assert rel_rms(out, ref) < 1e-2
+
+
 def _inputs(dit, rows, frames, C, seed=0):
     g = torch.Generator(device="cuda").manual_seed(seed)
     xs = [torch.randn(frames, C, device="cuda", generator=g, dtype=torch.float64) for _ in range(rows)]
