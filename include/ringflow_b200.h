@@ -177,6 +177,12 @@ int rf_decode_window(const double *latent, int64_t frames, int64_t channels,
                      int64_t overlap, int32_t full, int16_t *out, void *workspace,
                      int64_t workspace_bytes, void *stream);
 
+/* ToyCodec.encode (codec.py:168-174): latent[f, c] = sum_k samples[f*hop + k] * proj[c, k].
+ *   samples: device float64 [frames * hop]; proj_t: device [hop, C] (the reference's
+ *   encode_proj [C, hop], transposed); latent: device float64 [frames, C]. */
+int rf_encode_frames(const double *samples, int64_t frames, int64_t hop, const double *proj_t,
+                     int64_t channels, double *latent, void *stream);
+
 /* ------------------------------------------------------------ DiT GEMM (A8) ------
  * The tensor-core GEMM of the ACE-Step-shape DiT velocity model (the reference's
  * ToyFlowModel slot, model.py:91-152): out[M,N] = A[M,K] * B[N,K]^T with bf16 operands

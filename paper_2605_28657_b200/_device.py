@@ -40,7 +40,10 @@ def to_device_f64(x, dev=None) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = x.to(device=dev, dtype=torch.float64)
     else:
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to(dev)
+        a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+        if not a.flags.writeable:   # read-only views (CompletionRecord.latent): torch needs a writable buffer
+            a = a.copy()
+        t = torch.from_numpy(a).to(dev)
     return t.contiguous()
 
 

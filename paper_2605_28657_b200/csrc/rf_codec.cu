@@ -296,3 +296,51 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
     RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     return RF_OK;
 }
+
+// ------------------------------------------------------------------ encode (B-enc) ----
+// ToyCodec.encode (codec.py:168-174): latent[f, c] = sum_k samples[f * hop + k] * proj[c, k],
+// float64.  One CTA per frame: the frame's hop samples are staged in shared memory, thread c
+// accumulates channel c over k in ascending order with FMA (fixed order, so deterministic;
+// numpy's BLAS order differs, agreement to ~1e-15 relative).  proj_t is [hop, C] so the C
+// threads read consecutive doubles for each k.  Off the tick (source preparation), 2 C hop
+// FLOP per frame.
+namespace rf {
+__global__ void __launch_bounds__(128)
+rf_encode_kernel(const double *__restrict__ samples, int64_t hop, const double *__restrict__ proj_t, int channels,
+                 double *__restrict__ out) {
+    extern __shared__ double s_frame[];
+    const int64_t f = blockIdx.x;
+    for (int64_t k = threadIdx.x; k < hop; k += blockDim.x) s_frame[k] = samples[f * hop + k];
+    __syncthreads();
+    for (int c = threadIdx.x; c < channels; c += blockDim.x) {
+        double acc = 0.0;
+        for (int64_t k = 0; k < hop; ++k) acc = fma(s_frame[k], proj_t[k * channels + c], acc);
+        out[f * channels + c] = acc;
+    }
+}
+}  // namespace rf
+
+extern "C" int rf_encode_frames(const double *samples, int64_t frames, int64_t hop, const double *proj_t,
+                                int64_t channels, double *latent, void *stream) {
+    if (!samples || !proj_t || !latent || frames < 1 || hop < 1 || channels < 1 || channels > 1024) {
+        set_error("rf_encode_frames: bad arguments (frames=%lld hop=%lld C=%lld)", (long long)frames,
+                  (long long)hop, (long long)channels);
+        return RF_EINVAL;
+    }
+    const size_t smem = (size_t)hop * sizeof(double);
+    if (smem > 48 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            RF_TRY_CUDA(cudaFuncSetAttribute(rf_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        if (smem > 200 * 1024) {
+            set_error("rf_encode_frames: hop %lld too large", (long long)hop);
+            return RF_EINVAL;
+        }
+    }
+    rf_encode_kernel<<<(unsigned)frames, 128, smem, (cudaStream_t)stream>>>(samples, hop, proj_t, (int)channels,
+                                                                             latent);
+    RF_TRY_LAUNCH("rf_encode_kernel");
+    return RF_OK;
+}

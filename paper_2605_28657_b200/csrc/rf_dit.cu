@@ -177,6 +177,7 @@ struct Dit {
     __nv_bfloat16 *vt_self, *vt_cross;
     int n_pad, nc_pad;
     int64_t vt_cross_layer;                // elements per layer block of vt_cross
+    int skip = 0;                          // RF_DIT_SKIP at creation (timing ablation only)
     AttnPlan a_self;
     std::vector<AttnPlan> a_cross;
     RowPtrs *rows_dev;                       // per-call row inputs (rf_dit_set_rows)
@@ -285,6 +286,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     }
     Dit *d = new Dit();
     d->c = c;
+    d->skip = getenv("RF_DIT_SKIP") ? atoi(getenv("RF_DIT_SKIP")) : 0;
     d->w = *w;
     d->max_rows = max_rows;
     d->frames = frames;
@@ -394,10 +396,10 @@ static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shi
 // The forward body: a fixed launch sequence for a given row count and output buffer
 // (every per-call input is read from d.rows_dev), so it can be captured into a graph.
 static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
-    // RF_DIT_SKIP (timing ablation only; the output is garbage): bit mask of per-layer kernel
-    // classes left out -- 1 norms, 2 self-attention, 4 cross-attention, 8 QKV, 16 O, 32 cross-Q,
+    // RF_DIT_SKIP at rf_dit_create (timing ablation only; the output is garbage): bit mask of
+    // per-layer kernel classes left out -- 1 norms, 2 self-attention, 4 cross-attention, 8 QKV, 16 O, 32 cross-Q,
     // 64 cross-O, 128 gate-up, 256 down (tools/dit_ablate.py)
-    static const int skip = getenv("RF_DIT_SKIP") ? atoi(getenv("RF_DIT_SKIP")) : 0;
+    const int skip = d.skip;
     const rf_dit_config &c = d.c;
     const int64_t N = d.tokens, M = (int64_t)rows * N, D = c.d_model, L = c.n_layers, B = rows;
     const int64_t W6 = 6 * D, Nc = c.n_cond_tokens;

@@ -101,3 +101,17 @@ def test_pcm_chunk(rf, goldens):
         goldens["quantize_kat"].tolist()
     with pytest.raises(ValueError):
         rf.PcmChunk(np.zeros(10, dtype=np.int16), start_frame=0, hop=64)
+
+
+def test_encode_vs_reference(rf):
+    """ToyCodec.encode (codec.py:168-174) on the GPU (rf_encode_frames) vs the float64 numpy
+    product of the same projection; tolerance 1e-12 relative (summation order differs)."""
+    for C, hop in ((8, 64), (64, 1920)):
+        codec = rf.ToyCodec(channels=C, hop=hop)
+        x = scenarios.keyed(5, "encode-pcm", (37 * hop,))
+        lat = codec.encode(x)
+        ref = x.reshape(-1, hop) @ codec._encode_proj.T
+        assert lat.shape == (37, C) and lat.dtype == np.float64
+        assert np.max(np.abs(lat - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+    with pytest.raises(ValueError):
+        codec.encode(np.zeros(hop + 1))
