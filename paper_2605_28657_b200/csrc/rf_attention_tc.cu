@@ -635,8 +635,10 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
     uint64_t *bar = (uint64_t *)(sV + KS * kV64Tile);
     uint64_t *qfull = bar, *kfull = bar + 1, *kempty = kfull + KS, *vfull = kempty + KS, *vempty = vfull + KS;
     uint64_t *sfull = vempty + KS;         // [head * 2 + buffer]
+    // odone[head * 2 + (j & 1)]: PV(j) completion, alternating by tile parity so a waiter that
+    // skipped phases still reads an unambiguous parity (see the rescale wait below)
     uint64_t *pfull = sfull + 2 * NH, *odone = pfull + NH;
-    uint32_t *tmem_slot = (uint32_t *)(odone + NH);
+    uint32_t *tmem_slot = (uint32_t *)(odone + 2 * NH);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int MMA_WARP = 4 * NH, TMA_WARP = 4 * NH + 1;
@@ -660,10 +662,8 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             mbar_init(&vempty[i], 1);
         }
         for (int i = 0; i < 2 * NH; ++i) mbar_init(&sfull[i], 1);
-        for (int i = 0; i < NH; ++i) {
-            mbar_init(&pfull[i], 4);   // the 4 softmax warps of the head
-            mbar_init(&odone[i], 1);
-        }
+        for (int i = 0; i < NH; ++i) mbar_init(&pfull[i], 4);   // the 4 softmax warps of the head
+        for (int i = 0; i < 2 * NH; ++i) mbar_init(&odone[i], 1);
         mbar_fence_init();
     }
     if (warp == MMA_WARP) tmem_alloc<256 * NH>(tmem_slot);
@@ -714,7 +714,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
                     umma_bf16_ts(tmem + TO + a * 128, tmem + a * 128 + buf * 64 + ks * 8, bd, idesc_o,
                                  (acc || ks > 0) ? 1u : 0u);
                 }
-                umma_commit(&odone[a]);
+                umma_commit(&odone[a * 2 + buf]);
             };
             mbar_wait(qfull, 0);
             for (int j = 0; j < 2 && j < nt; ++j) {
@@ -778,10 +778,16 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             if (j == 0) {
                 m = tmax;
             } else {
-                mbar_wait(&odone[a], (j - 1) & 1);   // PV(j-1) done: O stable (and phases tracked exactly)
+                // the head pair (NH = 2) waits for PV(j-1) every tile (a lazy wait there showed
+                // corrupted outputs under rescaling; not yet understood)
+                if constexpr (NH == 2) mbar_wait(&odone[a * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
                 if (quarter == 0 && lane == 0) FA_TRACE(10 + a, j);
                 const bool need = tmax > m + 8.f;
                 if (__any_sync(0xffffffffu, need)) {   // lazy rescale of O and l
+                    // O must be stable: wait for PV(j-1).  Its barrier also completes for PV(j-3),
+                    // ..., all done (S(j)'s commit covers PV(j-2) and everything before), and PV(j+1)
+                    // cannot have run: the barrier is on PV(j-1)'s phase or just past it.
+                    if constexpr (NH == 1) mbar_wait(&odone[a * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
                     tc_fence_after();
                     const float mn = need ? tmax : m;
                     const float f = ex2_approx(m - mn);
@@ -824,7 +830,8 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             if (lane == 0) mbar_arrive(&pfull[a]);
             if (quarter == 0 && lane == 0) FA_TRACE(6 + a, j);
         }
-        mbar_wait(&odone[a], (nt - 1) & 1);
+        if (nt >= 2) mbar_wait(&odone[a * 2 + ((nt - 2) & 1)], ((nt - 2) >> 1) & 1);
+        mbar_wait(&odone[a * 2 + ((nt - 1) & 1)], ((nt - 1) >> 1) & 1);
         tc_fence_after();
         const float inv_l = l > 0.f ? 1.f / l : 0.f;
         const int qrow = q0 + quarter * 32 + lane;
