@@ -778,16 +778,13 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             if (j == 0) {
                 m = tmax;
             } else {
-                // the head pair (NH = 2) waits for PV(j-1) every tile (a lazy wait there showed
-                // corrupted outputs under rescaling; not yet understood)
-                if constexpr (NH == 2) mbar_wait(&odone[a * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
                 if (quarter == 0 && lane == 0) FA_TRACE(10 + a, j);
                 const bool need = tmax > m + 8.f;
                 if (__any_sync(0xffffffffu, need)) {   // lazy rescale of O and l
                     // O must be stable: wait for PV(j-1).  Its barrier also completes for PV(j-3),
                     // ..., all done (S(j)'s commit covers PV(j-2) and everything before), and PV(j+1)
                     // cannot have run: the barrier is on PV(j-1)'s phase or just past it.
-                    if constexpr (NH == 1) mbar_wait(&odone[a * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+                    mbar_wait(&odone[a * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
                     tc_fence_after();
                     const float mn = need ? tmax : m;
                     const float f = ex2_approx(m - mn);
@@ -828,6 +825,10 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&pfull[a]);
+            // keep the head's 4 warps within one tile of each other: pfull counts 4 arrivals per
+            // phase, so a warp that raced ahead and arrived for tile j + 1 before a slow warp's
+            // tile-j arrival would complete phase j early (PV(j) reading unfinished P rows)
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + a) : "memory");
             if (quarter == 0 && lane == 0) FA_TRACE(6 + a, j);
         }
         if (nt >= 2) mbar_wait(&odone[a * 2 + ((nt - 2) & 1)], ((nt - 2) >> 1) & 1);
