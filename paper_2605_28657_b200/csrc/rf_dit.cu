@@ -10,7 +10,8 @@
 //   qkv = a Wqkv^T, RoPE on q,k in the epilogue                       tcgen05 GEMM
 //   o   = Attention(q, k, v)                                          rf_attention
 //   h  += gate_msa[row] * (o Wo^T)                                    GEMM, gated-residual epi
-//   c   = RMSNorm(h);  oc = Attention(c Wqc^T, cond Wkc^T, cond Wvc^T)
+//   c   = RMSNorm(h);  oc = Attention(c Wqc^T, cond Wkc^T, cond Wvc^T)      (the norm fused:
+//         O-proj epilogue writes bf16(h) + row sums of squares, cross-Q epilogue scales rows)
 //   h  += oc Woc^T                                                    GEMM, residual epi
 //   m   = RMSNorm(h) * (1 + scale_mlp[row]) + shift_mlp[row]
 //   h  += gate_mlp[row] * (SwiGLU(m Wgu^T) Wdown^T)                   GEMM SwiGLU epi, GEMM
@@ -178,6 +179,11 @@ struct Dit {
     int n_pad, nc_pad;
     int64_t vt_cross_layer;                // elements per layer block of vt_cross
     int skip = 0;                          // RF_DIT_SKIP at creation (timing ablation only)
+    // the plain RMSNorm before the cross-attention query projection is fused across the GEMM
+    // boundary: the O projection's epilogue writes bf16(h) and per-128-column sums of squares,
+    // the cross-Q epilogue scales each row by its rsqrt(mean) (RF_DIT_FUSE_NORM=0: kernel)
+    bool fuse_norm2 = true;
+    float *sq_part = nullptr;              // [D / 128][max_rows * tokens]
     AttnPlan a_self;
     std::vector<AttnPlan> a_cross;
     RowPtrs *rows_dev;                       // per-call row inputs (rf_dit_set_rows)
@@ -220,7 +226,9 @@ static int64_t ws_layout(const rf_dit_config &c, int max_rows, int frames, Dit *
     void *vt_self = take((int64_t)max_rows * kv_dim * n_pad * 2);
     void *vt_cross = take((int64_t)c.n_layers * max_rows * kv_dim * nc_pad * 2);
     void *rows_dev = take(sizeof(RowPtrs));
+    void *sq_part = take((D / 128 + 1) * BN * 4);
     if (d) {
+        d->sq_part = (float *)sq_part;
         d->xin = (__nv_bfloat16 *)xin;
         d->a = (__nv_bfloat16 *)a;
         d->qkv = (__nv_bfloat16 *)qkv;
@@ -287,6 +295,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     Dit *d = new Dit();
     d->c = c;
     d->skip = getenv("RF_DIT_SKIP") ? atoi(getenv("RF_DIT_SKIP")) : 0;
+    d->fuse_norm2 = !(getenv("RF_DIT_FUSE_NORM") && atoi(getenv("RF_DIT_FUSE_NORM")) == 0) && c.d_model % 128 == 0;
     d->w = *w;
     d->max_rows = max_rows;
     d->frames = frames;
@@ -442,10 +451,27 @@ static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
         else
             RF_TRY(rf_attention_bf16(d.qkv, d.qkv + d.q_dim, d.qkv + d.q_dim + d.kv_dim, d.att, (int)B, (int)N,
                                      (int)N, c.n_heads, c.n_kv_heads, d.qkv_dim, d.qkv_dim, d.qkv_dim, d.q_dim, st));
-        if (!(skip & 16)) RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
+        NormFuse nf_out, nf_in;   // RMSNorm(h) for the cross-attention query, fused (see Dit)
+        if (d.fuse_norm2) {
+            const int64_t BNmax = (int64_t)d.max_rows * N;
+            nf_out.aux = d.a;
+            nf_out.aux_ld = D;
+            nf_out.sq_part = d.sq_part;
+            nf_out.sq_ld = BNmax;
+            nf_in.rs_part = d.sq_part;
+            nf_in.rs_ld = BNmax;
+            nf_in.rs_tiles = (int)(D / 128);
+            nf_in.rs_inv_d = 1.0f / (float)D;
+            nf_in.rs_eps = c.norm_eps;
+        }
+        if (!(skip & 16))
+            RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M,
+                            nullptr, d.fuse_norm2 ? &nf_out : nullptr));
         // cross-attention to the row's conditioning tokens (residual, no gate)
-        if (!(skip & 1)) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
-        if (!(skip & 32)) RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+        if (!(skip & 1) && !d.fuse_norm2) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
+        if (!(skip & 32))
+            RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M, nullptr,
+                            d.fuse_norm2 ? &nf_in : nullptr));
         const __nv_bfloat16 *kvl = d.kvc + l * 2 * d.kv_dim;
         if (skip & 4) {
         } else if (d.tc_attention)
@@ -512,3 +538,20 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
 }
 
 extern "C" float *rf_dit_output(void *handle) { return handle ? ((Dit *)handle)->vout : nullptr; }
+
+// Debugging aid (not part of the product ABI): change the timing-ablation mask of a live DiT
+// (see dit_body) and drop its captured graphs, so buffers keep the valid contents of earlier
+// full forwards while kernel classes are left out (tools/dit_ablate2.py).
+extern "C" int rf_dit_set_skip(void *handle, int32_t mask) {
+    Dit *d = (Dit *)handle;
+    if (!d) return RF_EINVAL;
+    cudaDeviceSynchronize();
+    d->skip = mask;
+    for (int i = 0; i <= kMaxDitRows; ++i)
+        if (d->graph[i]) {
+            cudaGraphExecDestroy(d->graph[i]);
+            d->graph[i] = nullptr;
+            d->graph_out[i] = nullptr;
+        }
+    return RF_OK;
+}

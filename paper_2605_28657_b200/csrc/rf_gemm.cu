@@ -88,6 +88,11 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
     return RF_OK;
 }
 
+static bool resid_two_pass() {   // RF_RESID_CC=64: two-pass residual epilogue at every K (tuning aid)
+    static const bool v = getenv("RF_RESID_CC") && atoi(getenv("RF_RESID_CC")) == 64;
+    return v;
+}
+
 template <int BN, int CG>
 static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStream_t st) {
     switch (epi) {
@@ -95,7 +100,7 @@ static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStre
         case gemm::kStoreF32: return launch<BN, gemm::kStoreF32, CG>(p, e, st);
         case gemm::kResidGate:
             // long K: the main loop hides a two-pass residual epilogue; keep the operand stages
-            if (BN == 128 && p.K >= 4096) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
+            if (BN == 128 && (p.K >= 4096 || resid_two_pass())) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
             return launch<BN, gemm::kResidGate, CG>(p, e, st);
         case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG>(p, e, st);
         case gemm::kStoreF32Scale: return launch<BN, gemm::kStoreF32Scale, CG>(p, e, st);
@@ -134,7 +139,7 @@ int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo) {
 
 int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,
              int rows_per_batch, float alpha, cudaStream_t st, const float2 *rope, int rope_cols, int64_t M,
-             const VtOut *vt) {
+             const VtOut *vt, const NormFuse *nf) {
     // The tensor maps cover the plan's (maximum) M; a smaller M only shortens the tile walk.
     GemmPlan p = plan;
     if (M > 0 && M < p.M) p.M = M;
@@ -146,6 +151,21 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
     gemm::EpiArgs e{out, ldo, gate, gate_ld, rows_per_batch > 0 ? rows_per_batch : 1, alpha, rope, rope_cols,
                     vt ? (__nv_bfloat16 *)vt->ptr : nullptr, vt ? vt->col0 : 0, vt ? vt->heads : 0,
                     vt ? vt->ld : 0, vt ? vt->period : 0, vt ? vt->layer_stride : 0, g_trace};
+    if (nf) {
+        if ((nf->aux && !(epi == gemm::kResidGate && p.bn == 128)) || (nf->rs_part && epi != gemm::kStoreBF16)) {
+            set_error("gemm: fused norm needs a BN=128 gated-residual producer / bf16-store consumer");
+            return RF_EINVAL;
+        }
+        e.aux = (__nv_bfloat16 *)nf->aux;
+        e.aux_ld = nf->aux_ld;
+        e.sq_part = nf->sq_part;
+        e.sq_ld = nf->sq_ld;
+        e.rs_part = nf->rs_part;
+        e.rs_ld = nf->rs_ld;
+        e.rs_tiles = nf->rs_tiles;
+        e.rs_inv_d = nf->rs_inv_d;
+        e.rs_eps = nf->rs_eps;
+    }
     if (p.bn == 256) return p.cg == 2 ? dispatch<256, 2>(p, epi, e, st) : dispatch<256, 1>(p, epi, e, st);
     return p.cg == 2 ? dispatch<128, 2>(p, epi, e, st) : dispatch<128, 1>(p, epi, e, st);
 }

@@ -50,6 +50,21 @@ struct EpiArgs {
     int64_t vt_layer_stride;
     // debugging: per-CTA clock64 timeline ([cta][tile < 16][8]); null in production
     unsigned long long *trace;
+    // RMSNorm fused across a GEMM boundary (the norm without modulation before the
+    // cross-attention query projection):
+    //  kResidGate (TMA-staged, BN = 128): with aux set, also aux[m * aux_ld + n] = bf16 of the
+    //    updated residual and sq_part[(n / 128) * sq_ld + m] = its sum of squares over the
+    //    tile's 128 columns (ascending column order);
+    //  kStoreBF16: with rs_part set, acc is scaled by rsqrt(sum_t rs_part[t * rs_ld + m] *
+    //    rs_inv_d + rs_eps) (t ascending) before rounding -- the consumer applies the norm.
+    __nv_bfloat16 *aux;
+    int64_t aux_ld;
+    float *sq_part;
+    int64_t sq_ld;
+    const float *rs_part;
+    int64_t rs_ld;
+    int rs_tiles;
+    float rs_inv_d, rs_eps;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -98,6 +113,10 @@ struct Cfg {
 };
 
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *(uint32_t *)&h;
+}
 
 template <int BN, int EPI, int CG = 1, int CC = BN>
 __global__ void __launch_bounds__(192, 1)
@@ -267,6 +286,9 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             ((float4 *)gs)[32 + lane] = __ldg((const float4 *)(epi.gate + (int64_t)b_hi * epi.gate_ld + n0) + lane);
             __syncwarp();
             const float *gr = gs + (m / epi.rows_per_batch != b_lo ? BN : 0);
+            const bool live = m0 + lane < M;
+            float ss = 0.f;
+            uint2 aux4[8];
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
@@ -291,6 +313,19 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         x.z += g4.z * __uint_as_float(r[4 * v + 2]);
                         x.w += g4.w * __uint_as_float(r[4 * v + 3]);
                         row[v ^ (lane & 7)] = x;
+                        if (epi.aux) {   // the next RMSNorm's input (bf16) and its partial sum
+                            ss = fmaf(x.x, x.x, ss);
+                            ss = fmaf(x.y, x.y, ss);
+                            ss = fmaf(x.z, x.z, ss);
+                            ss = fmaf(x.w, x.w, ss);
+                            aux4[v] = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+                        }
+                    }
+                    if (epi.aux && live) {
+                        uint4 *dst = (uint4 *)(epi.aux + (int64_t)(m0 + lane) * epi.aux_ld + n0 + col);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            dst[v] = make_uint4(aux4[2 * v].x, aux4[2 * v].y, aux4[2 * v + 1].x, aux4[2 * v + 1].y);
                     }
                 }
                 if (p == NP - 1) tc_fence_before();
@@ -317,6 +352,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                 }
             }
+            if (epi.aux && live) epi.sq_part[(int64_t)(n0 / BN) * epi.sq_ld + m0 + lane] = ss;
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -334,6 +370,14 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
             const int m = m0 + q * 32 + lane;
             const bool live = m < M;
+            float rs = 1.0f;   // fused RMSNorm of the A rows (kStoreBF16 with rs_part)
+            if constexpr (EPI == kStoreBF16) {
+                if (epi.rs_part && live) {
+                    float sum = 0.f;
+                    for (int t = 0; t < epi.rs_tiles; ++t) sum += epi.rs_part[(int64_t)t * epi.rs_ld + m];
+                    rs = rsqrtf(sum * epi.rs_inv_d + epi.rs_eps);
+                }
+            }
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t r[32];
@@ -349,8 +393,8 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         uint32_t *p = (uint32_t *)&pk;
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]),
-                                                                     __uint_as_float(r[v * 8 + 2 * e + 1]));
+                            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]) * rs,
+                                                                     __uint_as_float(r[v * 8 + 2 * e + 1]) * rs);
                             p[e] = *(uint32_t *)&h;
                         }
                         *(uint4 *)(o + v * 8) = pk;

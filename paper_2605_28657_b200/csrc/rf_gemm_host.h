@@ -33,9 +33,22 @@ struct VtOut {
     int64_t layer_stride = 0;   // elements between the groups' V^T blocks
 };
 
+// RMSNorm fused across a GEMM boundary (see gemm::EpiArgs): producer side (aux, sq_part) on
+// a TMA-staged gated-residual GEMM, consumer side (rs_part) on a bf16-store GEMM.
+struct NormFuse {
+    void *aux = nullptr;
+    int64_t aux_ld = 0;
+    float *sq_part = nullptr;
+    int64_t sq_ld = 0;
+    const float *rs_part = nullptr;
+    int64_t rs_ld = 0;
+    int rs_tiles = 0;
+    float rs_inv_d = 0.f, rs_eps = 0.f;
+};
+
 int gemm_run(const GemmPlan &p, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,
              int rows_per_batch, float alpha, cudaStream_t st, const float2 *rope = nullptr,
-             int rope_cols = 0, int64_t M = 0, const VtOut *vt = nullptr);
+             int rope_cols = 0, int64_t M = 0, const VtOut *vt = nullptr, const NormFuse *nf = nullptr);
 
 // tcgen05 attention (rf_attention_tc.cu): tensor maps over Q, K and V^T built once.
 struct AttnPlan {
