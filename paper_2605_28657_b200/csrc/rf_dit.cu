@@ -183,6 +183,10 @@ struct Dit {
     // boundary: the O projection's epilogue writes bf16(h) and per-128-column sums of squares,
     // the cross-Q epilogue scales each row by its rsqrt(mean) (RF_DIT_FUSE_NORM=0: kernel)
     bool fuse_norm2 = true;
+    // cross-attention computed in the epilogue of the cross-Q projection (single-CTA 128-row
+    // tiles per batch entry; RF_DIT_FUSE_XATTN=0: separate attention kernel)
+    bool fuse_xattn = true;
+    std::vector<GemmPlan> p_qcx;
     float *sq_part = nullptr;              // [D / 128][max_rows * tokens]
     AttnPlan a_self;
     std::vector<AttnPlan> a_cross;
@@ -296,6 +300,8 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     d->c = c;
     d->skip = getenv("RF_DIT_SKIP") ? atoi(getenv("RF_DIT_SKIP")) : 0;
     d->fuse_norm2 = !(getenv("RF_DIT_FUSE_NORM") && atoi(getenv("RF_DIT_FUSE_NORM")) == 0) && c.d_model % 128 == 0;
+    d->fuse_xattn = !(getenv("RF_DIT_FUSE_XATTN") && atoi(getenv("RF_DIT_FUSE_XATTN")) == 0) && c.head_dim == 128 &&
+                    c.n_cond_tokens <= 128;
     d->w = *w;
     d->max_rows = max_rows;
     d->frames = frames;
@@ -326,6 +332,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     d->p_qkv.resize(L);
     d->p_o.resize(L);
     d->p_qc.resize(L);
+    d->p_qcx.resize(L);
     d->p_oc.resize(L);
     d->p_gu.resize(L);
     d->p_down.resize(L);
@@ -337,6 +344,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
         plan(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_qc[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D);
+        if (!rc) rc = gemm_plan(&d->p_qcx[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D, D, D, 128, 1);
         plan(&d->p_oc[l], d->att, woc + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_gu[l], d->a, wgu + l * 2 * (int64_t)c.mlp_hidden * D, BN, 2 * (int64_t)c.mlp_hidden, D);
         plan(&d->p_down[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, BN, D, c.mlp_hidden);
@@ -469,11 +477,18 @@ static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
                             nullptr, d.fuse_norm2 ? &nf_out : nullptr));
         // cross-attention to the row's conditioning tokens (residual, no gate)
         if (!(skip & 1) && !d.fuse_norm2) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
-        if (!(skip & 32))
+        const bool xattn = d.fuse_xattn && d.tc_attention;
+        if (xattn && !(skip & 32)) {   // query projection + cross-attention in one kernel
+            const XAttn xa{&d.a_cross[l].tk, &d.a_cross[l].tvt, (int)N, (int)B, (int)Nc,
+                           c.n_heads / c.n_kv_heads, c.n_kv_heads};
+            RF_TRY(gemm_run(d.p_qcx[l], 6 /* cross-attention epilogue */, d.att, d.q_dim, nullptr, 0, 1, 1.f, st,
+                            nullptr, 0, M, nullptr, d.fuse_norm2 ? &nf_in : nullptr, &xa));
+        } else if (!(skip & 32)) {
             RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M, nullptr,
                             d.fuse_norm2 ? &nf_in : nullptr));
+        }
         const __nv_bfloat16 *kvl = d.kvc + l * 2 * d.kv_dim;
-        if (skip & 4) {
+        if ((skip & 4) || xattn) {
         } else if (d.tc_attention)
             RF_TRY(attn_run(d.a_cross[l], d.att, d.q_dim, (int)B, st));
         else

@@ -66,7 +66,9 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
         RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         attr = true;
     }
-    const int tiles = (int)((p.M + gemm::BM * CG - 1) / (gemm::BM * CG)) * (int)(p.N / BN);
+    const int tiles = (EPI == gemm::kCrossAttn ? e.x_batches * e.x_mtpb
+                                               : (int)((p.M + gemm::BM * CG - 1) / (gemm::BM * CG))) *
+                      (int)(p.N / BN);
     int units = sm_count() / CG;   // persistent: one CTA (pair) per SM (pair)
     if (tiles < units) units = tiles;
     cudaLaunchConfig_t cfg = {};
@@ -83,7 +85,7 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = CG == 2 ? 2 : 1;
-    RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, (int)p.M, (int)p.N, (int)p.K, e));
+    RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, p.tk, p.tvt, (int)p.M, (int)p.N, (int)p.K, e));
     RF_TRY_LAUNCH("rf_gemm_kernel");
     return RF_OK;
 }
@@ -139,7 +141,7 @@ int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo) {
 
 int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,
              int rows_per_batch, float alpha, cudaStream_t st, const float2 *rope, int rope_cols, int64_t M,
-             const VtOut *vt, const NormFuse *nf) {
+             const VtOut *vt, const NormFuse *nf, const XAttn *xa) {
     // The tensor maps cover the plan's (maximum) M; a smaller M only shortens the tile walk.
     GemmPlan p = plan;
     if (M > 0 && M < p.M) p.M = M;
@@ -152,7 +154,7 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
                     vt ? (__nv_bfloat16 *)vt->ptr : nullptr, vt ? vt->col0 : 0, vt ? vt->heads : 0,
                     vt ? vt->ld : 0, vt ? vt->period : 0, vt ? vt->layer_stride : 0, g_trace};
     if (nf) {
-        if ((nf->aux && !(epi == gemm::kResidGate && p.bn == 128)) || (nf->rs_part && epi != gemm::kStoreBF16)) {
+        if ((nf->aux && !(epi == gemm::kResidGate && p.bn == 128)) || (nf->rs_part && epi != gemm::kStoreBF16 && epi != gemm::kCrossAttn)) {
             set_error("gemm: fused norm needs a BN=128 gated-residual producer / bf16-store consumer");
             return RF_EINVAL;
         }
@@ -165,6 +167,23 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
         e.rs_tiles = nf->rs_tiles;
         e.rs_inv_d = nf->rs_inv_d;
         e.rs_eps = nf->rs_eps;
+    }
+    if (epi == gemm::kCrossAttn) {
+        if (!xa || p.bn != 128 || p.cg != 1 || xa->n_keys > 128 || xa->n_keys < 1 || xa->rows_per_batch < 1 ||
+            p.N % 128) {
+            set_error("gemm: cross-attention epilogue needs 128-wide single-CTA tiles and <= 128 keys");
+            return RF_EINVAL;
+        }
+        p.tk = *xa->tk;
+        p.tvt = *xa->tvt;
+        e.x_rpb = xa->rows_per_batch;
+        e.x_mtpb = (xa->rows_per_batch + gemm::BM - 1) / gemm::BM;
+        e.x_batches = xa->batches;
+        e.x_nk = xa->n_keys;
+        e.x_group = xa->group;
+        e.x_hkv = xa->kv_heads;
+        e.x_scale = 1.4426950408889634f / sqrtf(128.f);
+        return launch<128, gemm::kCrossAttn, 1>(p, e, st);
     }
     if (p.bn == 256) return p.cg == 2 ? dispatch<256, 2>(p, epi, e, st) : dispatch<256, 1>(p, epi, e, st);
     return p.cg == 2 ? dispatch<128, 2>(p, epi, e, st) : dispatch<128, 1>(p, epi, e, st);

@@ -26,6 +26,8 @@ enum Epi : int {
     kSwiGLU = 3,      // columns interleaved (g, u): out(bf16)[m, n/2] = silu(g) * u
     kStoreF32Scale = 4,  // out(f32)[m,n] = alpha * acc
     kBF16Rope = 5,    // out(bf16)[m,n] = acc, interleaved-pair RoPE on columns < rope_cols
+    kCrossAttn = 6,   // acc = one 128-column query head of 128 rows -> cross-attention in the
+                      // epilogue: out(bf16)[m, head cols] = softmax(q K_b^T / sqrt(128)) V_b
 };
 
 struct EpiArgs {
@@ -65,6 +67,11 @@ struct EpiArgs {
     int64_t rs_ld;
     int rs_tiles;
     float rs_inv_d, rs_eps;
+    // kCrossAttn: rows are tiled per batch entry (x_rpb rows each, x_mtpb tiles of 128), so a
+    // tile's rows all attend to the same batch entry's x_nk keys (K via tma_k, V^T via tma_vt,
+    // the attention kernel's maps); query head = n / 128, KV head = head / x_group.
+    int x_rpb, x_mtpb, x_batches, x_nk, x_group, x_hkv;
+    float x_scale;   // log2(e) / sqrt(head dim)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -103,9 +110,10 @@ struct Cfg {
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN_LOAD * BK * 2;
     static constexpr bool TMA_C = EPI == 2 && BN == 128;
+    static constexpr bool XATT = EPI == 6;   // Q, K, V^T staging (32 KB each) for the epilogue attention
     static constexpr int C_COLS = CC;                                           // staged per pass
     static constexpr uint32_t C_WARP_BYTES = TMA_C ? 32u * C_COLS * 4u : 0u;   // per epilogue warp
-    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + (TMA_C ? 4u * 1024u : 0u);   // + gate rows
+    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + (TMA_C ? 4u * 1024u : 0u) + (XATT ? 3u * 32768u : 0u);
     // as many operand stages as fit next to the epilogue staging (227 KB opt-in limit)
     static constexpr uint32_t BUDGET = 232448u - 1024u - 512u - C_BYTES;
     static constexpr int STAGES = (int)(BUDGET / (A_BYTES + B_BYTES)) > 10 ? 10 : (int)(BUDGET / (A_BYTES + B_BYTES));
@@ -121,7 +129,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 template <int BN, int EPI, int CG = 1, int CC = BN>
 __global__ void __launch_bounds__(192, 1)
 rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-               const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, EpiArgs epi) {
+               const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_k,
+               const __grid_constant__ CUtensorMap tma_vt, int M, int N, int K, EpiArgs epi) {
     using namespace rf::sm100;
     using C = Cfg<BN, CG, EPI, CC>;
     constexpr int TM = BM * CG;   // output rows per tile (per CTA pair when CG = 2)
@@ -136,7 +145,10 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *cfull = tempty + 2;            // [4] one per epilogue warp (TMA_C)
-    uint32_t *tmem_slot = (uint32_t *)(cfull + 4);
+    uint64_t *xbar = cfull + 4;              // [3] kCrossAttn: K/V loaded, S done, O done
+    uint32_t *tmem_slot = (uint32_t *)(xbar + 3);
+    static_assert(!C::XATT || (CG == 1 && BN == 128), "cross-attention epilogue: single-CTA 128-wide tiles");
+    constexpr uint32_t TMEM_COLS = C::XATT ? 512 : 2 * BN;   // + S and O of the epilogue attention
 
     RF_GTRACE(15);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,13 +166,18 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             mbar_init(&tempty[i], 4 * CG);   // the epilogue warps of both CTAs release the leader
         }
         for (int i = 0; i < 4; ++i) mbar_init(&cfull[i], 1);
+        for (int i = 0; i < 3; ++i) mbar_init(&xbar[i], 1);
+        if constexpr (C::XATT) {
+            tma_prefetch(&tma_k);
+            tma_prefetch(&tma_vt);
+        }
         mbar_fence_init();
     }
     if (warp == 1) {
         if constexpr (CG == 2)
-            tmem_alloc_pair<2 * BN>(tmem_slot);
+            tmem_alloc_pair<TMEM_COLS>(tmem_slot);
         else
-            tmem_alloc<2 * BN>(tmem_slot);
+            tmem_alloc<TMEM_COLS>(tmem_slot);
     }
     tc_fence_before();
     if constexpr (CG == 2)
@@ -173,7 +190,13 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     pdl_launch();
     RF_GTRACE(13);
 
-    const int num_m = (M + TM - 1) / TM, num_n = N / BN, kblocks = K / BK;
+    const int num_m = C::XATT ? epi.x_batches * epi.x_mtpb : (M + TM - 1) / TM, num_n = N / BN, kblocks = K / BK;
+    // first row of tile t (kCrossAttn: tiles never straddle two batch entries)
+    auto row0 = [&](int t) {
+        const int mt = t % num_m;
+        if constexpr (C::XATT) return (mt / epi.x_mtpb) * epi.x_rpb + (mt % epi.x_mtpb) * BM;
+        return mt * TM + (int)rank * BM;
+    };
     const int num_tiles = num_m * num_n;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile walker id
     const int units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
@@ -184,7 +207,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             uint32_t phase = 0;
             int it = 0;
             for (int t = unit; t < num_tiles; t += units, ++it) {
-                const int m0 = (t % num_m) * TM + (int)rank * BM, n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
+                const int m0 = row0(t), n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
                 RF_TRACE(it, 6);
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -359,12 +382,164 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             }
         }
         if (lane == 0) bulk_wait0();
+    } else if constexpr (C::XATT) {
+        // Cross-attention in the epilogue of the query projection.  Per tile (128 rows of one
+        // batch entry x one query head): Q (accumulator, fused-norm scaled) -> bf16 SW128 tile
+        // in smem; S = Q K^T (128 x 128, issued by one epilogue thread into TMEM columns
+        // 256..383 while the MMA warp already runs the next tile's main loop); row softmax
+        // (one row per thread, a single key tile: no rescaling); P (bf16) over S in TMEM;
+        // O = P V (TS MMA into columns 384..511); O / l -> bf16 att.  K and V^T of the next
+        // tile are prefetched by TMA as soon as this tile's MMAs have read them.
+        const int q = warp & 3;
+        const int row = q * 32 + lane;                       // row within the tile
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        uint8_t *sQ = sC, *sK = sC + 32768, *sV = sC + 65536;
+        uint64_t *xk = xbar, *xs = xbar + 1, *xo = xbar + 2;
+        const bool leader = q == 0 && lane == 0;
+        constexpr uint32_t idS = idesc_bf16(128, 128);
+        auto load_kv = [&](int t) {
+            const int mt = t % num_m, b = mt / epi.x_mtpb, hk = (t / num_m) / epi.x_group;
+            mbar_expect_tx(xk, 65536);
+            tma_load_2d(sK, &tma_k, xk, hk * 128, b * epi.x_nk);
+            tma_load_2d(sK + 16384, &tma_k, xk, hk * 128 + 64, b * epi.x_nk);
+            tma_load_2d(sV, &tma_vt, xk, 0, (b * epi.x_hkv + hk) * 128);
+            tma_load_2d(sV + 16384, &tma_vt, xk, 64, (b * epi.x_hkv + hk) * 128);
+        };
+        auto epi_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+        int acc = 0, it = 0;
+        uint32_t acc_phase = 0, xph = 0;
+        if (leader && unit < num_tiles) load_kv(unit);
+        for (int t = unit; t < num_tiles; t += units, ++it) {
+            const int m0 = row0(t), n0 = (t / num_m) * BN;
+            const int valid = min(BM, epi.x_rpb - ((t % num_m) % epi.x_mtpb) * BM);
+            const bool live = row < valid && m0 + row < M;
+            float rs = 1.0f;   // the fused RMSNorm of the query projection's input rows
+            if (epi.rs_part && live) {
+                float sum = 0.f;
+                for (int tt = 0; tt < epi.rs_tiles; ++tt) sum += epi.rs_part[(int64_t)tt * epi.rs_ld + m0 + row];
+                rs = rsqrtf(sum * epi.rs_inv_d + epi.rs_eps);
+            }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            if (q == 2 && lane == 0) RF_TRACE(it, 4);
+            // Q row -> bf16, K-major SW128 (two [128 rows][64 dims] halves)
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
+                tmem_ld_wait();
+                uint8_t *half = sQ + (c >> 1) * 16384 + row * 128;
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    const uint4 w = make_uint4(
+                        pack_bf16(__uint_as_float(r[8 * qq]) * rs, __uint_as_float(r[8 * qq + 1]) * rs),
+                        pack_bf16(__uint_as_float(r[8 * qq + 2]) * rs, __uint_as_float(r[8 * qq + 3]) * rs),
+                        pack_bf16(__uint_as_float(r[8 * qq + 4]) * rs, __uint_as_float(r[8 * qq + 5]) * rs),
+                        pack_bf16(__uint_as_float(r[8 * qq + 6]) * rs, __uint_as_float(r[8 * qq + 7]) * rs));
+                    const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
+                    *(uint4 *)(half + chunk * 16) = w;
+                }
+            }
+            tc_fence_before();
+            fence_proxy_async_smem();   // Q (generic proxy) -> visible to the tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);   // the accumulator is free for tile i + 2
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+            epi_sync();
+            if (leader) {
+                mbar_wait(xk, xph);
+                tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t ad = sdesc_sw128(sQ + (ks >> 2) * 16384) + (uint64_t)((ks & 3) * 2);
+                    const uint64_t bd = sdesc_sw128(sK + (ks >> 2) * 16384) + (uint64_t)((ks & 3) * 2);
+                    umma_bf16(tmem + 256, ad, bd, idS, ks > 0);
+                }
+                umma_commit(xs);
+            }
+            mbar_wait(xs, xph);
+            tc_fence_after();
+            uint32_t sr[128];
+            tmem_ld32(tmem + lane_base + 256, *(uint32_t(*)[32])(sr));
+            tmem_ld32(tmem + lane_base + 288, *(uint32_t(*)[32])(sr + 32));
+            tmem_ld32(tmem + lane_base + 320, *(uint32_t(*)[32])(sr + 64));
+            tmem_ld32(tmem + lane_base + 352, *(uint32_t(*)[32])(sr + 96));
+            tmem_ld_wait();
+            if (epi.x_nk < 128) {
+#pragma unroll
+                for (int e = 0; e < 128; ++e)
+                    if (e >= epi.x_nk) sr[e] = __float_as_uint(-INFINITY);
+            }
+            float mx[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) mx[u] = fmaxf(__uint_as_float(sr[u]), __uint_as_float(sr[u + 4]));
+#pragma unroll
+            for (int e = 8; e < 128; e += 8)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    mx[u] = fmaxf(mx[u], fmaxf(__uint_as_float(sr[e + u]), __uint_as_float(sr[e + u + 4])));
+            const float nm = -fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * epi.x_scale;
+            float l = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    float p0, p1;
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(sr[c * 32 + 2 * e]), epi.x_scale, nm)));
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(sr[c * 32 + 2 * e + 1]), epi.x_scale, nm)));
+                    l += p0 + p1;
+                    pk[e] = pack_bf16(p0, p1);
+                }
+                tmem_st16(tmem + lane_base + 256 + c * 16, pk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            epi_sync();
+            if (leader) {
+                tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t bd = sdesc_sw128(sV + (ks >> 2) * 16384) + (uint64_t)((ks & 3) * 2);
+                    umma_bf16_ts(tmem + 384, tmem + 256 + ks * 8, bd, idS, ks > 0);
+                }
+                umma_commit(xo);
+            }
+            mbar_wait(xo, xph);
+            tc_fence_after();
+            xph ^= 1;
+            // S and PV have read Q, K and V: prefetch the next tile's K / V^T
+            if (leader && t + units < num_tiles) load_kv(t + units);
+            const float inv_l = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem + lane_base + 384 + c * 32, r);
+                tmem_ld_wait();
+                if (live) {
+                    __nv_bfloat16 *dst = (__nv_bfloat16 *)epi.out + (int64_t)(m0 + row) * epi.ldo + n0 + c * 32;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        *(uint4 *)(dst + v * 8) = make_uint4(
+                            pack_bf16(__uint_as_float(r[v * 8]) * inv_l, __uint_as_float(r[v * 8 + 1]) * inv_l),
+                            pack_bf16(__uint_as_float(r[v * 8 + 2]) * inv_l, __uint_as_float(r[v * 8 + 3]) * inv_l),
+                            pack_bf16(__uint_as_float(r[v * 8 + 4]) * inv_l, __uint_as_float(r[v * 8 + 5]) * inv_l),
+                            pack_bf16(__uint_as_float(r[v * 8 + 6]) * inv_l, __uint_as_float(r[v * 8 + 7]) * inv_l));
+                }
+            }
+            tc_fence_before();
+            epi_sync();   // O read by every warp before the next tile's PV overwrites it
+            if (q == 2 && lane == 0) RF_TRACE(it, 5);
+        }
     } else {
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         int acc = 0, it = 0;
         uint32_t acc_phase = 0;
         for (int t = unit; t < num_tiles; t += units, ++it) {
-            const int m0 = (t % num_m) * TM + (int)rank * BM, n0 = (t / num_m) * BN;
+            const int m0 = row0(t), n0 = (t / num_m) * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
@@ -503,10 +678,10 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     if constexpr (CG == 2) {
         tc_fence_before();
         cluster_sync();   // the leader's MMAs and commits into this CTA are done
-        if (warp == 1) tmem_dealloc_pair<2 * BN>(tmem);
+        if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem);
     } else {
         __syncthreads();
-        if (warp == 1) tmem_dealloc<2 * BN>(tmem);
+        if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
     }
     RF_GTRACE(14);
 }

@@ -9,6 +9,7 @@ namespace rf {
 struct GemmPlan {
     CUtensorMap ta, tb;
     CUtensorMap tc;             // fp32 output map of the TMA-staged residual epilogue
+    CUtensorMap tk, tvt;        // K / V^T maps of the cross-attention epilogue (RF_EPI_XATTN)
     void *c_ptr = nullptr;
     int64_t c_ld = 0, c_rows = 0;
     int64_t M, N, K;
@@ -46,9 +47,17 @@ struct NormFuse {
     float rs_inv_d = 0.f, rs_eps = 0.f;
 };
 
+// Cross-attention in the query projection's epilogue (gemm::kCrossAttn): rows_per_batch
+// query rows per batch entry, n_keys keys per entry, K / V^T through the attention maps.
+struct XAttn {
+    const CUtensorMap *tk, *tvt;
+    int rows_per_batch, batches, n_keys, group, kv_heads;
+};
+
 int gemm_run(const GemmPlan &p, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,
              int rows_per_batch, float alpha, cudaStream_t st, const float2 *rope = nullptr,
-             int rope_cols = 0, int64_t M = 0, const VtOut *vt = nullptr, const NormFuse *nf = nullptr);
+             int rope_cols = 0, int64_t M = 0, const VtOut *vt = nullptr, const NormFuse *nf = nullptr,
+             const XAttn *xa = nullptr);
 
 // tcgen05 attention (rf_attention_tc.cu): tensor maps over Q, K and V^T built once.
 struct AttnPlan {

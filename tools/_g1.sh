@@ -1,7 +1,7 @@
-O=gpurun_out/r1zm; mkdir -p $O
-timeout 600 python -m pytest tests/test_gpu_dit.py tests/test_gpu_gemm.py -x -q > $O/pytest.txt 2>&1
-tail -2 $O/pytest.txt
-timeout 120 python tools/dit_check.py 4 > $O/check.txt 2>&1; head -1 $O/check.txt
-RF_DIT_FUSE_NORM=0 timeout 120 python tools/dit_check.py 4 > $O/check0.txt 2>&1; head -1 $O/check0.txt
-timeout 1200 python tools/ab.py "RF_DIT_FUSE_NORM=1" "RF_DIT_FUSE_NORM=0" --rounds=5 > $O/ab.txt 2>&1
-cat $O/ab.txt
+O=gpurun_out/r1zp; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
+tail -n 3 $O/pytest_gpu.log $O/smoke.log; python -c "
+import json; d=json.load(open('$O/bench.json')); print(d['value'], d['ms_per_step'], d['phase_ms'], d['roofline']['frac'], d['e2e']['value'], d['clocks'], d['toy_path']['value'], d['cpu_baseline']['value'])"
+tail -n 3 $O/bench.err
