@@ -193,6 +193,7 @@ struct Dit {
     RowPtrs *rows_dev;                       // per-call row inputs (rf_dit_set_rows)
     // one CUDA graph of the forward body per row count (and output buffer)
     cudaGraphExec_t graph[kMaxDitRows + 1] = {};
+    int graph_kernels[kMaxDitRows + 1] = {};   // kernel nodes of each captured forward
     float *graph_out[kMaxDitRows + 1] = {};
     bool use_graphs;
     bool tc_attention;
@@ -542,6 +543,8 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
             return rc;
         }
         RF_TRY_CUDA(ce);
+        size_t nodes = 0;
+        if (cudaGraphGetNodes(g, nullptr, &nodes) == cudaSuccess) d.graph_kernels[rows] = (int)nodes;
         const cudaError_t ie = cudaGraphInstantiate(&d.graph[rows], g, 0);
         cudaGraphDestroy(g);
         RF_TRY_CUDA(ie);
@@ -569,4 +572,12 @@ extern "C" int rf_dit_set_skip(void *handle, int32_t mask) {
             d->graph_out[i] = nullptr;
         }
     return RF_OK;
+}
+
+// Kernels one forward of `rows` rows launches (the row-table kernel + the captured graph's
+// kernel nodes); -1 before that row count's graph exists.  Reported by bench.py.
+extern "C" int rf_dit_launches(void *handle, int32_t rows) {
+    Dit *d = (Dit *)handle;
+    if (!d || rows < 1 || rows > d->max_rows || !d->graph[rows]) return -1;
+    return 1 + d->graph_kernels[rows];
 }

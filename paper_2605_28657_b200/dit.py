@@ -52,6 +52,8 @@ def _declare(lib):
                                   ctypes.POINTER(vp), vp]
     lib.rf_dit_destroy.restype = ctypes.c_int
     lib.rf_dit_destroy.argtypes = [vp]
+    lib.rf_dit_launches.restype = ctypes.c_int
+    lib.rf_dit_launches.argtypes = [vp, i32]
     lib.rf_dit_forward.restype = ctypes.c_int
     lib.rf_dit_forward.argtypes = [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_float), ctypes.POINTER(vp),
                                    vp, vp]
@@ -302,8 +304,13 @@ class DiTVelocity:
         self.dit = dit
         self.uncond_prompt = uncond_prompt
         self._p = _Pending()
-        # kernels per forward (csrc/rf_dit.cu): 9 conditioning + in-proj + 12 per layer + 2 final
-        self.launches_per_forward = 12 + 12 * dit.cfg.n_layers
+        self._last_rows = 0
+
+    @property
+    def launches_per_forward(self) -> int:
+        """Kernels the last forward launched (counted from its captured CUDA graph)."""
+        n = self.dit.lib.rf_dit_launches(self.dit.handle, self._last_rows) if self._last_rows else 0
+        return max(n, 0)
 
     def _row(self, x, t, prompt_hash) -> int:
         self._p.xs.append(x)
@@ -331,4 +338,5 @@ class DiTVelocity:
     def forward(self, pipe) -> None:
         p, self._p = self._p, _Pending()
         if p.xs:
+            self._last_rows = len(p.xs)
             self.dit.forward(p.xs, p.ts, p.conds)
