@@ -39,6 +39,29 @@ inline int pdl_allowed() {
     return v;
 }
 
+// L2 residency window: while set (the DiT forward sets it to its fp32 residual stream),
+// every kernel launched through launch_pdl / the GEMM launcher carries an access-policy
+// window marking that range persisting in L2, so the residual stream read and rewritten
+// by three epilogues per layer stays on chip instead of round-tripping through HBM.
+struct L2Window {
+    void *base = nullptr;
+    size_t bytes = 0;
+    float hit_ratio = 0.f;
+};
+inline L2Window g_l2_window;
+
+// appends the window attribute (if any) to at[n]; returns the new attribute count
+inline unsigned add_l2_window(cudaLaunchAttribute *at, unsigned n) {
+    if (!g_l2_window.base) return n;
+    at[n].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[n].val.accessPolicyWindow.base_ptr = g_l2_window.base;
+    at[n].val.accessPolicyWindow.num_bytes = g_l2_window.bytes;
+    at[n].val.accessPolicyWindow.hitRatio = g_l2_window.hit_ratio;
+    at[n].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[n].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    return n + 1;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args &&...args) {
@@ -47,11 +70,11 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = add_l2_window(at, 1);
     return cudaLaunchKernelEx(&cfg, kern, static_cast<Args &&>(args)...);
 }
 

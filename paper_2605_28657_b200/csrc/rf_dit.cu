@@ -197,6 +197,7 @@ struct Dit {
     float *graph_out[kMaxDitRows + 1] = {};
     bool use_graphs;
     bool tc_attention;
+    L2Window l2win;   // the residual stream h, kept persisting in L2 during the forward
     // GEMM plans (tensor maps at max rows)
     GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out, p_kvc;
     std::vector<GemmPlan> p_qkv, p_o, p_qc, p_oc, p_gu, p_down;
@@ -373,6 +374,22 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         return rc;
     }
     d->tc_attention = getenv("RF_ATTN_MMA_SYNC") == nullptr;   // the tcgen05 kernel is the default
+    // L2 persistence for the fp32 residual stream (24.6 MB at 4 rows; RF_DIT_L2_PERSIST=0 off)
+    if (!(getenv("RF_DIT_L2_PERSIST") && atoi(getenv("RF_DIT_L2_PERSIST")) == 0)) {
+        int dev = 0, maxp = 0;
+        const size_t hb = (size_t)max_rows * d->tokens * c.d_model * sizeof(float);
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && maxp > 0) {
+            size_t lim = hb < (size_t)maxp ? hb : (size_t)maxp, cur = 0;
+            if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur > lim) lim = cur;
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim) == cudaSuccess) {
+                d->l2win.base = d->h;
+                d->l2win.bytes = hb;
+                d->l2win.hit_ratio = lim >= hb ? 1.0f : (float)lim / (float)hb;
+            }
+        }
+        cudaGetLastError();   // attribute / limit queries are best-effort
+    }
     d->use_graphs = getenv("RF_DIT_NO_GRAPH") == nullptr;
     // V^T pad columns are never written: zero them once
     RF_TRY_CUDA(cudaMemsetAsync(d->vt_self, 0, (size_t)max_rows * d->kv_dim * d->n_pad * 2, (cudaStream_t)stream));
@@ -413,7 +430,14 @@ static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shi
 
 // The forward body: a fixed launch sequence for a given row count and output buffer
 // (every per-call input is read from d.rows_dev), so it can be captured into a graph.
+static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st);
 static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
+    g_l2_window = d.l2win;   // every launch below carries the residual stream's L2 window
+    const int rc = dit_body_(d, rows, v_out, st);
+    g_l2_window = L2Window{};
+    return rc;
+}
+static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
     // RF_DIT_SKIP at rf_dit_create (timing ablation only; the output is garbage): bit mask of
     // per-layer kernel classes left out -- 1 norms, 2 self-attention, 4 cross-attention, 8 QKV, 16 O, 32 cross-Q,
     // 64 cross-O, 128 gate-up, 256 down (tools/dit_ablate.py)

@@ -57,17 +57,17 @@ static int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dt, const void *pt
     return RF_OK;
 }
 
-template <int BN, int EPI, int CG, int CC = BN>
+template <int BN, int EPI, int CG, int CC = BN, int MT = 1>
 static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
-    using C = gemm::Cfg<BN, CG, EPI, CC>;
-    auto kern = gemm::rf_gemm_kernel<BN, EPI, CG, CC>;
+    using C = gemm::Cfg<BN, CG, EPI, CC, MT>;
+    auto kern = gemm::rf_gemm_kernel<BN, EPI, CG, CC, MT>;
     static bool attr = false;
     if (!attr) {
         RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         attr = true;
     }
     const int tiles = (EPI == gemm::kCrossAttn ? e.x_batches * e.x_mtpb
-                                               : (int)((p.M + gemm::BM * CG - 1) / (gemm::BM * CG))) *
+                                               : (int)((p.M + gemm::BM * CG * MT - 1) / (gemm::BM * CG * MT))) *
                       (int)(p.N / BN);
     int units = sm_count() / CG;   // persistent: one CTA (pair) per SM (pair)
     if (tiles < units) units = tiles;
@@ -76,7 +76,7 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
     cfg.blockDim = dim3(192);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait()
     at[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
     at[1].id = cudaLaunchAttributeClusterDimension;
@@ -84,7 +84,7 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
     at[1].val.clusterDim.y = 1;
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = CG == 2 ? 2 : 1;
+    cfg.numAttrs = add_l2_window(at, CG == 2 ? 2 : 1);
     RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, p.tk, p.tvt, (int)p.M, (int)p.N, (int)p.K, e));
     RF_TRY_LAUNCH("rf_gemm_kernel");
     return RF_OK;
@@ -95,8 +95,26 @@ static bool resid_two_pass() {   // RF_RESID_CC=64: two-pass residual epilogue a
     return v;
 }
 
+// two m-subtiles per CTA (BN = 256 pair tiles of 512 x 256): register epilogues only
+template <int BN, int CG>
+static int dispatch_mt2(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStream_t st) {
+    switch (epi) {
+        case gemm::kStoreBF16: return launch<BN, gemm::kStoreBF16, CG, BN, 2>(p, e, st);
+        case gemm::kStoreF32: return launch<BN, gemm::kStoreF32, CG, BN, 2>(p, e, st);
+        case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG, BN, 2>(p, e, st);
+        case gemm::kBF16Rope: return launch<BN, gemm::kBF16Rope, CG, BN, 2>(p, e, st);
+    }
+    set_error("gemm: epilogue %d has no two-subtile variant", epi);
+    return RF_EINVAL;
+}
+
 template <int BN, int CG>
 static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStream_t st) {
+    if (p.mt == 2) {
+        if constexpr (BN == 256 && CG == 2) return dispatch_mt2<BN, CG>(p, epi, e, st);
+        set_error("gemm: two m-subtiles need 256-wide pair tiles");
+        return RF_EINVAL;
+    }
     switch (epi) {
         case gemm::kStoreBF16: return launch<BN, gemm::kStoreBF16, CG>(p, e, st);
         case gemm::kStoreF32: return launch<BN, gemm::kStoreF32, CG>(p, e, st);
@@ -113,12 +131,14 @@ static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStre
 }
 
 int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, int64_t K, int64_t lda,
-              int64_t ldb, int bn, int cg) {
-    if (K % gemm::BK || (bn != 128 && bn != 256) || (cg != 1 && cg != 2) || N % bn || M < 1) {
-        set_error("gemm: unsupported shape M=%lld N=%lld K=%lld BN=%d CG=%d", (long long)M, (long long)N,
-                  (long long)K, bn, cg);
+              int64_t ldb, int bn, int cg, int mt) {
+    if (K % gemm::BK || (bn != 128 && bn != 256) || (cg != 1 && cg != 2) || N % bn || M < 1 ||
+        (mt != 1 && !(mt == 2 && bn == 256 && cg == 2))) {
+        set_error("gemm: unsupported shape M=%lld N=%lld K=%lld BN=%d CG=%d MT=%d", (long long)M, (long long)N,
+                  (long long)K, bn, cg, mt);
         return RF_EINVAL;
     }
+    p->mt = mt;
     p->M = M;
     p->N = N;
     p->K = K;
@@ -202,13 +222,15 @@ extern "C" int rf_gemm_bf16(const void *A, const void *B, void *out, int64_t M, 
                             int64_t gate_ld, int32_t rows_per_batch, float alpha, int32_t block_n,
                             void *stream) {
     // block_n: 128 / 256 = one CTA per 128 x block_n tile; -128 / -256 = a CTA pair
-    // (cta_group::2) per 256 x |block_n| tile
+    // (cta_group::2) per 256 x |block_n| tile; -(256 + 4096) = a CTA pair per 512 x 256 tile
+    // (two m-subtiles per CTA)
     if (!A || !B || !out || (epilogue == gemm::kResidGate && !gate) || epilogue == gemm::kBF16Rope) {
         set_error("rf_gemm_bf16: null argument");
         return RF_EINVAL;
     }
     GemmPlan p;
-    int rc = gemm_plan(&p, A, B, M, N, K, lda, ldb, block_n < 0 ? -block_n : block_n, block_n < 0 ? 2 : 1);
+    const int mag = block_n < 0 ? -block_n : block_n;
+    int rc = gemm_plan(&p, A, B, M, N, K, lda, ldb, mag & 4095, block_n < 0 ? 2 : 1, 1 + (mag >> 12));
     if (rc) return rc;
     return gemm_run(p, epilogue, out, ldo, gate, gate_ld, rows_per_batch, alpha, (cudaStream_t)stream);
 }

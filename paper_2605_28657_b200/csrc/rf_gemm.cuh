@@ -104,11 +104,12 @@ constexpr int BM = 128, BK = 64;
 // CC: residual columns staged per pass (BN: one pass per tile; 64: two passes, half the
 // staging memory, two more operand stages -- for long K, where the main loop hides the
 // epilogue anyway and latency tolerance matters more).
-template <int BN, int CG = 1, int EPI = 0, int CC = BN>
+template <int BN, int CG = 1, int EPI = 0, int CC = BN, int MT = 1>
 struct Cfg {
     static constexpr int BN_LOAD = BN / CG;   // B rows staged by each CTA
-    static constexpr uint32_t A_BYTES = BM * BK * 2;
+    static constexpr uint32_t A_BYTES = BM * BK * 2;   // one m-subtile of A per CTA
     static constexpr uint32_t B_BYTES = BN_LOAD * BK * 2;
+    static constexpr uint32_t STAGE_BYTES = MT * A_BYTES + B_BYTES;
     static constexpr bool TMA_C = EPI == 2 && BN == 128;
     static constexpr bool XATT = EPI == 6;   // Q, K, V^T staging (32 KB each) for the epilogue attention
     static constexpr int C_COLS = CC;                                           // staged per pass
@@ -116,8 +117,13 @@ struct Cfg {
     static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + (TMA_C ? 4u * 1024u : 0u) + (XATT ? 3u * 32768u : 0u);
     // as many operand stages as fit next to the epilogue staging (227 KB opt-in limit)
     static constexpr uint32_t BUDGET = 232448u - 1024u - 512u - C_BYTES;
-    static constexpr int STAGES = (int)(BUDGET / (A_BYTES + B_BYTES)) > 10 ? 10 : (int)(BUDGET / (A_BYTES + B_BYTES));
-    static constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + 512;
+    static constexpr int STAGES = (int)(BUDGET / STAGE_BYTES) > 10 ? 10 : (int)(BUDGET / STAGE_BYTES);
+    static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + C_BYTES + 512;
+    // TMEM: MT m-subtiles x BN columns per accumulator; two accumulators when they fit
+    // (the epilogue of tile i overlaps the main loop of tile i+1), else one whose halves
+    // are released separately (see the MMA warp).
+    static constexpr int ACC_COLS = MT * BN;
+    static constexpr int NACC = 2 * ACC_COLS <= 512 ? 2 : 1;
 };
 
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
@@ -126,19 +132,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *(uint32_t *)&h;
 }
 
-template <int BN, int EPI, int CG = 1, int CC = BN>
+template <int BN, int EPI, int CG = 1, int CC = BN, int MT = 1>
 __global__ void __launch_bounds__(192, 1)
 rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_k,
                const __grid_constant__ CUtensorMap tma_vt, int M, int N, int K, EpiArgs epi) {
     using namespace rf::sm100;
-    using C = Cfg<BN, CG, EPI, CC>;
-    constexpr int TM = BM * CG;   // output rows per tile (per CTA pair when CG = 2)
+    using C = Cfg<BN, CG, EPI, CC, MT>;
+    constexpr int TM = BM * CG;   // output rows per m-subtile (per CTA pair when CG = 2)
+    constexpr int ACC_COLS = C::ACC_COLS, NACC = C::NACC;
     constexpr int STAGES = C::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = base;
-    uint8_t *sB = base + STAGES * C::A_BYTES;
+    uint8_t *sB = base + STAGES * MT * C::A_BYTES;   // A: [stage][m-subtile]
     uint8_t *sC = sB + STAGES * C::B_BYTES;   // C_BYTES (1024-aligned: stage sizes are multiples of 1 KB)
     uint64_t *full = (uint64_t *)(sC + C::C_BYTES);
     uint64_t *empty = full + STAGES;
@@ -148,7 +155,8 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     uint64_t *xbar = cfull + 4;              // [3] kCrossAttn: K/V loaded, S done, O done
     uint32_t *tmem_slot = (uint32_t *)(xbar + 3);
     static_assert(!C::XATT || (CG == 1 && BN == 128), "cross-attention epilogue: single-CTA 128-wide tiles");
-    constexpr uint32_t TMEM_COLS = C::XATT ? 512 : 2 * BN;   // + S and O of the epilogue attention
+    static_assert(MT == 1 || (!C::TMA_C && !C::XATT), "two m-subtiles: register epilogues only");
+    constexpr uint32_t TMEM_COLS = C::XATT ? 512 : NACC * ACC_COLS;   // + S and O of the epilogue attention
 
     RF_GTRACE(15);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -190,12 +198,13 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     pdl_launch();
     RF_GTRACE(13);
 
-    const int num_m = C::XATT ? epi.x_batches * epi.x_mtpb : (M + TM - 1) / TM, num_n = N / BN, kblocks = K / BK;
-    // first row of tile t (kCrossAttn: tiles never straddle two batch entries)
-    auto row0 = [&](int t) {
+    const int num_m = C::XATT ? epi.x_batches * epi.x_mtpb : (M + TM * MT - 1) / (TM * MT), num_n = N / BN,
+              kblocks = K / BK;
+    // first row of m-subtile j of tile t (kCrossAttn: tiles never straddle two batch entries)
+    auto row0 = [&](int t, int j = 0) {
         const int mt = t % num_m;
         if constexpr (C::XATT) return (mt / epi.x_mtpb) * epi.x_rpb + (mt % epi.x_mtpb) * BM;
-        return mt * TM + (int)rank * BM;
+        return (mt * MT + j) * TM + (int)rank * BM;
     };
     const int num_tiles = num_m * num_n;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile walker id
@@ -207,19 +216,23 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             uint32_t phase = 0;
             int it = 0;
             for (int t = unit; t < num_tiles; t += units, ++it) {
-                const int m0 = row0(t), n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
+                const int n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
                 RF_TRACE(it, 6);
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if constexpr (CG == 2) {
                         // both CTAs' bytes complete on the leader's full barrier
-                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
                         const uint32_t fb = mapa_shared(&full[stage], 0);
-                        tma_load_2d_pair(sA + stage * C::A_BYTES, &tma_a, fb, kb * BK, m0);
+#pragma unroll
+                        for (int j = 0; j < MT; ++j)
+                            tma_load_2d_pair(sA + (stage * MT + j) * C::A_BYTES, &tma_a, fb, kb * BK, row0(t, j));
                         tma_load_2d_pair(sB + stage * C::B_BYTES, &tma_b, fb, kb * BK, n0);
                     } else {
-                        mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
-                        tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * BK, m0);
+                        mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+#pragma unroll
+                        for (int j = 0; j < MT; ++j)
+                            tma_load_2d(sA + (stage * MT + j) * C::A_BYTES, &tma_a, &full[stage], kb * BK, row0(t, j));
                         tma_load_2d(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0);
                     }
                     if (++stage == STAGES) {
@@ -235,42 +248,79 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             int it = 0;
+            // MMAs of one k block into m-subtile j's accumulator columns
+            auto issue = [&](int stg, int kb, int j) {
+                const uint32_t d_tmem = tmem + acc * ACC_COLS + j * BN;
+                const uint64_t ad = sdesc_sw128(sA + (stg * MT + j) * C::A_BYTES);
+                const uint64_t bd = sdesc_sw128(sB + stg * C::B_BYTES);
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k) {
+                    if constexpr (CG == 2)
+                        umma_bf16_pair(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+                    else
+                        umma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+                }
+            };
+            auto release = [&](int stg) {
+                if constexpr (CG == 2)
+                    umma_commit_pair(&empty[stg]);
+                else
+                    umma_commit(&empty[stg]);
+            };
+            auto advance = [](int &stg, uint32_t &ph) {
+                if (++stg == STAGES) {
+                    stg = 0;
+                    ph ^= 1;
+                }
+            };
             for (int t = unit; t < num_tiles; t += units, ++it) {
                 RF_TRACE(it, 0);
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                RF_TRACE(it, 1);
-                const uint32_t d_tmem = tmem + acc * BN;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                int kb0 = 0;
+                if constexpr (NACC == 1 && MT == 2) {
+                    // One accumulator: the epilogue releases m-subtile 0's columns first.  Run
+                    // subtile 0's MMAs over the first `lag` k blocks while subtile 1 drains,
+                    // then catch subtile 1 up on the same (still resident) stages.
+                    const int lag = kblocks < STAGES ? kblocks : STAGES;
+                    mbar_wait(&tempty[0], acc_phase ^ 1);
+                    tc_fence_after();
+                    RF_TRACE(it, 1);
+                    int s2 = stage;
+                    uint32_t p2 = phase;
+                    for (int kb = 0; kb < lag; ++kb) {
+                        mbar_wait(&full[s2], p2);
+                        tc_fence_after();
+                        if (kb == 0) RF_TRACE(it, 2);
+                        issue(s2, kb, 0);
+                        advance(s2, p2);
+                    }
+                    mbar_wait(&tempty[1], acc_phase ^ 1);
+                    tc_fence_after();
+                    for (int kb = 0; kb < lag; ++kb) {
+                        issue(stage, kb, 1);
+                        release(stage);
+                        advance(stage, phase);
+                    }
+                    kb0 = lag;
+                } else {
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    tc_fence_after();
+                    RF_TRACE(it, 1);
+                }
+                for (int kb = kb0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (kb == 0) RF_TRACE(it, 2);
-                    const uint64_t ad = sdesc_sw128(sA + stage * C::A_BYTES);
-                    const uint64_t bd = sdesc_sw128(sB + stage * C::B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        if constexpr (CG == 2)
-                            umma_bf16_pair(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
-                                           (kb | k) != 0);
-                        else
-                            umma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
-                                      (kb | k) != 0);
-                    }
-                    if constexpr (CG == 2)
-                        umma_commit_pair(&empty[stage]);
-                    else
-                        umma_commit(&empty[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    for (int j = 0; j < MT; ++j) issue(stage, kb, j);
+                    release(stage);
+                    advance(stage, phase);
                 }
                 RF_TRACE(it, 3);
                 if constexpr (CG == 2)
                     umma_commit_pair(&tfull[acc]);
                 else
                     umma_commit(&tfull[acc]);
-                if (++acc == 2) {
+                if (++acc == NACC) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
@@ -539,10 +589,13 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         int acc = 0, it = 0;
         uint32_t acc_phase = 0;
         for (int t = unit; t < num_tiles; t += units, ++it) {
-            const int m0 = row0(t), n0 = (t / num_m) * BN;
+            const int n0 = (t / num_m) * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
+#pragma unroll 1
+          for (int j = 0; j < MT; ++j) {
+            const int m0 = row0(t, j);
             const int m = m0 + q * 32 + lane;
             const bool live = m < M;
             float rs = 1.0f;   // fused RMSNorm of the A rows (kStoreBF16 with rs_part)
@@ -553,10 +606,41 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     rs = rsqrtf(sum * epi.rs_inv_d + epi.rs_eps);
                 }
             }
+            // kBF16Rope: this thread's token row of the (cos, sin) table, one 16-pair block
+            // (8 float4) per 32-column chunk.  Chunks h * 128 + pb * 32 of the tile's heads
+            // share block pb, so chunks are walked pb-major and block pb + 1 is prefetched
+            // while block pb is applied (the table row is an L2 read; a load per use
+            // stalled the epilogue behind the main loop).
+            constexpr int NCH = BN / 32;
+            constexpr int NH = EPI == kBF16Rope ? BN / 128 : 1;
+            float4 tc[8], tn[8];
+            const float4 *tab = nullptr;
+            bool tile_rot = false;
+            if constexpr (EPI == kBF16Rope) {
+                tile_rot = n0 < epi.rope_cols;
+                tab = (const float4 *)(epi.rope + (int64_t)(m % epi.rows_per_batch) * 64);
+                if (tile_rot) {
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) tc[v] = __ldg(tab + v);
+                }
+            }
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int ci = 0; ci < NCH; ++ci) {
+                const int c0 = EPI == kBF16Rope ? (ci % NH) * 128 + (ci / NH) * 32 : ci * 32;
+                if constexpr (EPI == kBF16Rope) {
+                    if (tile_rot && ci % NH == 0) {
+                        if (ci > 0) {
+#pragma unroll
+                            for (int v = 0; v < 8; ++v) tc[v] = tn[v];
+                        }
+                        if (ci + NH < NCH) {
+#pragma unroll
+                            for (int v = 0; v < 8; ++v) tn[v] = __ldg(tab + (ci / NH + 1) * 8 + v);
+                        }
+                    }
+                }
                 uint32_t r[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * ACC_COLS + j * BN + c0), r);
                 tmem_ld_wait();
                 if (!live) continue;
                 const int n = n0 + c0;
@@ -589,7 +673,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                     __nv_bfloat16 *o = (__nv_bfloat16 *)epi.out + (int64_t)m * epi.ldo + n;
                     const bool rot = n < epi.rope_cols;
-                    const float2 *cs = epi.rope + (int64_t)(m % epi.rows_per_batch) * 64 + ((n & 127) >> 1);
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         uint4 pk;
@@ -601,7 +684,8 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                                 // q/k are bf16 Linear outputs: round, then rotate in fp32
                                 x0 = bf16_round(x0);
                                 x1 = bf16_round(x1);
-                                const float2 c = cs[v * 4 + e];
+                                const float4 c4 = tc[v * 2 + (e >> 1)];
+                                const float2 c = (e & 1) ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
                                 const float y0 = x0 * c.x - x1 * c.y, y1 = x0 * c.y + x1 * c.x;
                                 x0 = y0;
                                 x1 = y1;
@@ -651,7 +735,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                             // gate/up rounded to bf16 like a bf16 Linear output, then SiLU(g)*u
                             const float gt = bf16_round(__uint_as_float(r[4 * e + 2 * h]));
                             const float up = bf16_round(__uint_as_float(r[4 * e + 2 * h + 1]));
-                            y[h] = gt / (1.0f + __expf(-gt)) * up;
+                            y[h] = __fdividef(gt, 1.0f + __expf(-gt)) * up;   // fast divide: 2 ulp, far below bf16
                         }
                         __nv_bfloat162 hh = __floats2bfloat162_rn(y[0], y[1]);
                         p[e] = *(uint32_t *)&hh;
@@ -660,16 +744,29 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     *(uint4 *)(o + 8) = pk[1];
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (q == 2) RF_TRACE(it, 5);
-                if constexpr (CG == 2)
-                    mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
-                else
-                    mbar_arrive(&tempty[acc]);
+            if constexpr (NACC == 1) {   // one accumulator: release m-subtile j's columns now
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2)
+                        mbar_arrive_cluster(mapa_shared(&tempty[j], 0));
+                    else
+                        mbar_arrive(&tempty[j]);
+                }
             }
-            if (++acc == 2) {
+          }
+            if constexpr (NACC == 2) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2)
+                        mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+                    else
+                        mbar_arrive(&tempty[acc]);
+                }
+            }
+            if (q == 2 && lane == 0) RF_TRACE(it, 5);
+            if (++acc == NACC) {
                 acc = 0;
                 acc_phase ^= 1;
             }

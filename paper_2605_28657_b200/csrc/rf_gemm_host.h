@@ -15,6 +15,7 @@ struct GemmPlan {
     int64_t M, N, K;
     int bn;
     int cg;   // 1: 128 x bn tiles per CTA; 2: 256 x bn tiles per CTA pair (cta_group::2)
+    int mt = 1;   // 2: two 256-row m-subtiles per pair tile (512 x 256; bn = 256, cg = 2)
 };
 
 int make_tmap_bf16_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes,
@@ -24,7 +25,7 @@ int make_tmap_f32_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t
 // bind the residual-stream output of a kResidGate plan (builds its TMA map once)
 int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo);
 int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, int64_t K, int64_t lda,
-              int64_t ldb, int bn, int cg = 1);
+              int64_t ldb, int bn, int cg = 1, int mt = 1);
 // Transposed V output of the QKV / cross-KV GEMM (see EpiArgs::vt).
 struct VtOut {
     void *ptr;

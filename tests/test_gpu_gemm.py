@@ -65,3 +65,29 @@ def test_gemm_swiglu(ops, pair):
     g, u = ref(a, wg).bfloat16().float(), ref(a, wu).bfloat16().float()
     r = torch.nn.functional.silu(g) * u
     assert torch.allclose(out.float(), r, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(3000, 12288, 2048), (3000, 4096, 2048), (100, 256, 64), (700, 512, 128),
+                                   (513, 256, 320), (6000, 2048, 6144), (1, 256, 64)])
+def test_gemm_two_m_subtiles_bit_identical(ops, M, N, K):
+    """512 x 256 pair tiles (two m-subtiles share each weight stage; one TMEM accumulator
+    whose halves are released separately) give the same bits as 256 x 256 pair tiles: each
+    output element is the same K-ordered tcgen05 accumulation."""
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    base = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=256, pair=True)
+    two = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=256, pair=True, m_subtiles=2)
+    assert torch.equal(base, two)
+    r = ref(a, b)
+    assert (two - r).abs().max().item() <= 1e-5 * r.abs().max().item()
+
+
+def test_gemm_two_m_subtiles_swiglu(ops):
+    M, K, H = 3000, 2048, 6144
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(2 * H, K, device="cuda", generator=g) * 0.02).bfloat16()
+    base = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256, pair=True)
+    two = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256, pair=True, m_subtiles=2)
+    assert torch.equal(base, two)
