@@ -353,6 +353,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         // gated-residual outputs all update h: bind it once (TMA map of the epilogue)
         for (GemmPlan *g : {&d->p_o[l], &d->p_oc[l], &d->p_down[l]})
             if (!rc && g->bn == 128) rc = gemm_plan_c(g, d->h, D);
+        if (!rc && d->p_gu[l].bn == 256) rc = gemm_plan_o(&d->p_gu[l], d->mlp, c.mlp_hidden);
     }
     // the cross-attention K/V projections of all layers read the same conditioning tokens:
     // one [rows * n_cond, L * 2 * kv_dim] GEMM per forward instead of L narrow ones

@@ -159,6 +159,14 @@ int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo) {
     return make_tmap_f32_2d(&p->tc, out, (uint64_t)p->N, (uint64_t)p->M, (uint64_t)ldo * 4, 32, 32);
 }
 
+int gemm_plan_o(GemmPlan *p, void *out, int64_t ldo) {
+    p->c_ptr = out;
+    p->c_ld = ldo;
+    p->c_rows = p->M;
+    // bf16 [M, N / 2] SwiGLU output, 64 x 32 boxes (128-byte rows: SWIZZLE_128B)
+    return make_tmap_bf16_2d(&p->tc, out, (uint64_t)(p->N / 2), (uint64_t)p->M, (uint64_t)ldo * 2, 64, 32);
+}
+
 int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float *gate, int64_t gate_ld,
              int rows_per_batch, float alpha, cudaStream_t st, const float2 *rope, int rope_cols, int64_t M,
              const VtOut *vt, const NormFuse *nf, const XAttn *xa) {
@@ -168,6 +176,11 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
     if (epi == gemm::kResidGate && p.bn == 128 && (p.c_ptr != out || p.c_ld != ldo || p.c_rows != p.M)) {
         // the TMA-staged residual epilogue needs a map over `out` (cached when planned)
         int rc = gemm_plan_c(&p, out, ldo);
+        if (rc) return rc;
+    }
+    if (epi == gemm::kSwiGLU && p.bn == 256 && p.mt == 1 && (p.c_ptr != out || p.c_ld != ldo || p.c_rows != p.M)) {
+        // the TMA-stored SwiGLU epilogue needs a map over `out` (cached when planned)
+        int rc = gemm_plan_o(&p, out, ldo);
         if (rc) return rc;
     }
     gemm::EpiArgs e{out, ldo, gate, gate_ld, rows_per_batch > 0 ? rows_per_batch : 1, alpha, rope, rope_cols,

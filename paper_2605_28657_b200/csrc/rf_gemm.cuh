@@ -112,8 +112,12 @@ struct Cfg {
     static constexpr uint32_t STAGE_BYTES = MT * A_BYTES + B_BYTES;
     static constexpr bool TMA_C = EPI == 2 && BN == 128;
     static constexpr bool XATT = EPI == 6;   // Q, K, V^T staging (32 KB each) for the epilogue attention
+    // TMA_O (SwiGLU, BN = 256): each epilogue warp stages its [32 rows][128 cols] bf16 output
+    // in shared memory (two SWIZZLE_128B boxes of 64 columns) and writes it with TMA stores:
+    // full-line writes instead of one 16-byte store per row per thread
+    static constexpr bool TMA_O = EPI == 3 && BN == 256 && MT == 1;
     static constexpr int C_COLS = CC;                                           // staged per pass
-    static constexpr uint32_t C_WARP_BYTES = TMA_C ? 32u * C_COLS * 4u : 0u;   // per epilogue warp
+    static constexpr uint32_t C_WARP_BYTES = TMA_C ? 32u * C_COLS * 4u : (TMA_O ? 32u * 128u * 2u : 0u);
     static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + (TMA_C ? 4u * 1024u : 0u) + (XATT ? 3u * 32768u : 0u);
     // as many operand stages as fit next to the epilogue staging (227 KB opt-in limit)
     static constexpr uint32_t BUDGET = 232448u - 1024u - 512u - C_BYTES;
@@ -164,7 +168,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
-        if constexpr (C::TMA_C) tma_prefetch(&tma_c);
+        if constexpr (C::TMA_C || C::TMA_O) tma_prefetch(&tma_c);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -613,6 +617,10 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             // stalled the epilogue behind the main loop).
             constexpr int NCH = BN / 32;
             constexpr int NH = EPI == kBF16Rope ? BN / 128 : 1;
+            if constexpr (C::TMA_O) {   // the previous tile's stores have read the staging buffer
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+            }
             float4 tc[8], tn[8];
             const float4 *tab = nullptr;
             bool tile_rot = false;
@@ -724,7 +732,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         *(float4 *)(o + v * 4) = x;
                     }
                 } else if constexpr (EPI == kSwiGLU) {
-                    __nv_bfloat16 *o = (__nv_bfloat16 *)epi.out + (int64_t)m * epi.ldo + n / 2;
                     uint4 pk[2];
                     uint32_t *p = (uint32_t *)pk;
 #pragma unroll
@@ -740,8 +747,17 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         __nv_bfloat162 hh = __floats2bfloat162_rn(y[0], y[1]);
                         p[e] = *(uint32_t *)&hh;
                     }
-                    *(uint4 *)o = pk[0];
-                    *(uint4 *)(o + 8) = pk[1];
+                    if constexpr (C::TMA_O) {
+                        // output columns ci * 16 .. + 15: box ci / 4, 16-byte chunks 2 (ci % 4) + {0, 1}
+                        uint8_t *box = sC + q * C::C_WARP_BYTES + (ci >> 2) * 4096 + lane * 128;
+                        const int ch = (ci & 3) * 2;
+                        *(uint4 *)(box + (((ch) ^ (lane & 7)) << 4)) = pk[0];
+                        *(uint4 *)(box + (((ch + 1) ^ (lane & 7)) << 4)) = pk[1];
+                    } else {
+                        __nv_bfloat16 *o = (__nv_bfloat16 *)epi.out + (int64_t)m * epi.ldo + n / 2;
+                        *(uint4 *)o = pk[0];
+                        *(uint4 *)(o + 8) = pk[1];
+                    }
                 }
             }
             if constexpr (NACC == 1) {   // one accumulator: release m-subtile j's columns now
@@ -765,12 +781,25 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         mbar_arrive(&tempty[acc]);
                 }
             }
+            if constexpr (C::TMA_O) {   // rows >= M are clipped by the tensor map
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const int orow = row0(t) + q * 32;
+                    tma_store_2d(&tma_c, sC + q * C::C_WARP_BYTES, n0 / 2, orow);
+                    tma_store_2d(&tma_c, sC + q * C::C_WARP_BYTES + 4096, n0 / 2 + 64, orow);
+                    bulk_commit();
+                }
+            }
             if (q == 2 && lane == 0) RF_TRACE(it, 5);
             if (++acc == NACC) {
                 acc = 0;
                 acc_phase ^= 1;
             }
         }
+    }
+    if constexpr (C::TMA_O) {
+        if (warp >= 2 && lane == 0) bulk_wait0();
     }
     if constexpr (CG == 2) {
         tc_fence_before();

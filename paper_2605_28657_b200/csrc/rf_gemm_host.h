@@ -24,6 +24,8 @@ int make_tmap_f32_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t
                      uint32_t box_inner, uint32_t box_outer);
 // bind the residual-stream output of a kResidGate plan (builds its TMA map once)
 int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo);
+// bind the bf16 output of a SwiGLU plan with 256-wide tiles (TMA-stored epilogue)
+int gemm_plan_o(GemmPlan *p, void *out, int64_t ldo);
 int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, int64_t K, int64_t lda,
               int64_t ldb, int bn, int cg = 1, int mt = 1);
 // Transposed V output of the QKV / cross-KV GEMM (see EpiArgs::vt).
