@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-toy", action="store_true")
+    ap.add_argument("--no-library-baseline", action="store_true")
     return ap.parse_args()
 
 
@@ -310,6 +311,17 @@ def run_ours(args):
 
     long_decode = decode_240s(codec, world, rank, flush, hbm_peak)
 
+    # ---- the same DiT forward written with library kernels (cuBLAS GEMMs + SDPA) ----
+    library = None
+    if not args.no_library_baseline and rank == 0:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import dit_torch_baseline
+
+        library = dit_torch_baseline.compare(rows=DEPTH, check=False)
+        library["what"] = ("config-2 DiT forward (4 rows) in stock PyTorch: cuBLAS bf16 GEMMs, SDPA attention, "
+                           "torch elementwise norms/RoPE/SwiGLU, one CUDA graph (tools/dit_torch_baseline.py); "
+                           "native = this repo's tcgen05 forward on the same weights")
+
     # ---------------- toy-velocity leg (the reference's own model) ----------------
     toy = None
     if not args.no_toy:
@@ -368,7 +380,7 @@ def run_ours(args):
         "roofline": {"bound": "tensor", "kernel": "dit_forward (tcgen05 GEMMs + attention + norms, one launch set)",
                      "achieved": round(dit_tflops, 1), "peak": bf16_sust, "unit": "TFLOP/s",
                      "frac": round(dit_tflops / bf16_sust, 4), "traffic": forward_traffic()[0],
-                     "traffic_note": "DRAM read+write bytes of one forward (sum over its 279 launches) from the "
+                     "traffic_note": "DRAM read+write bytes of one forward (sum over its launches) from the "
                                      "committed ncu launch list profiles/r1_dit_forward_traffic.json, "
                                      f"--cache-control none; cold-cache sum {forward_traffic()[1]}",
                      "algorithmic_flops_per_launch": dit_flops,
@@ -378,6 +390,8 @@ def run_ours(args):
     }
     if toy is not None:
         line["toy_path"] = toy
+    if library is not None:
+        line["library_baseline"] = library
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, processes=1)
     print(json.dumps(line), flush=True)

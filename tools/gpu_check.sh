@@ -10,4 +10,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -k regex:'rf_|gemm' -c 700 --csv --log-file $O/dit_launches.csv python tools/dit_check.py 4 --no-ref > $O/ncu_dit.log 2>&1
-tail -3 $O/pytest_gpu.log $O/smoke.log; cat $O/bench.json; tail -3 $O/bench.err
+tail -n 3 $O/pytest_gpu.log $O/smoke.log; cat $O/bench.json; tail -3 $O/bench.err
