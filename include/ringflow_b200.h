@@ -191,8 +191,8 @@ int rf_encode_frames(const double *samples, int64_t frames, int64_t hop, const d
  *   out[m,n] += gate[(m / rows_per_batch) * gate_ld + n] * acc, 3 = SwiGLU over
  *   interleaved (gate, up) columns -> bf16 out[m, n/2], 4 = store f32 * alpha.
  * K % 64 == 0, N % block_n == 0, block_n in {128, 256}: one CTA per 128 x block_n tile;
- * -block_n: a CTA pair (cta_group::2) per 256 x block_n tile; -(256 + 4096): a CTA pair per
- * 512 x 256 tile (two 256-row m-subtiles share each staged B tile; not for epilogue 2). */
+ * -block_n: a CTA pair (cta_group::2) per 256 x block_n tile; |block_n| + 4096: stream-K
+ * tile walk (equal k-block shares per persistent CTA; split tiles summed in a fixed order). */
 #define RF_EPI_BF16 0
 #define RF_EPI_F32 1
 #define RF_EPI_RESID_GATE 2

@@ -57,20 +57,21 @@ static int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dt, const void *pt
     return RF_OK;
 }
 
-template <int BN, int EPI, int CG, int CC = BN, int MT = 1>
+template <int BN, int EPI, int CG, int CC = BN>
 static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
-    using C = gemm::Cfg<BN, CG, EPI, CC, MT>;
-    auto kern = gemm::rf_gemm_kernel<BN, EPI, CG, CC, MT>;
+    using C = gemm::Cfg<BN, CG, EPI, CC>;
+    auto kern = gemm::rf_gemm_kernel<BN, EPI, CG, CC>;
     static bool attr = false;
     if (!attr) {
         RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
         attr = true;
     }
     const int tiles = (EPI == gemm::kCrossAttn ? e.x_batches * e.x_mtpb
-                                               : (int)((p.M + gemm::BM * CG * MT - 1) / (gemm::BM * CG * MT))) *
+                                               : (int)((p.M + gemm::BM * CG - 1) / (gemm::BM * CG))) *
                       (int)(p.N / BN);
     int units = sm_count() / CG;   // persistent: one CTA (pair) per SM (pair)
-    if (tiles < units) units = tiles;
+    // stream-K splits the PLAN's k-block range over all units, whatever this call's M
+    if (tiles < units && !e.sk_ws) units = tiles;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(units * CG));
     cfg.blockDim = dim3(192);
@@ -95,33 +96,20 @@ static bool resid_two_pass() {   // RF_RESID_CC=64: two-pass residual epilogue a
     return v;
 }
 
-// two m-subtiles per CTA (BN = 256 pair tiles of 512 x 256): register epilogues only
-template <int BN, int CG>
-static int dispatch_mt2(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStream_t st) {
-    switch (epi) {
-        case gemm::kStoreBF16: return launch<BN, gemm::kStoreBF16, CG, BN, 2>(p, e, st);
-        case gemm::kStoreF32: return launch<BN, gemm::kStoreF32, CG, BN, 2>(p, e, st);
-        case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG, BN, 2>(p, e, st);
-        case gemm::kBF16Rope: return launch<BN, gemm::kBF16Rope, CG, BN, 2>(p, e, st);
-    }
-    set_error("gemm: epilogue %d has no two-subtile variant", epi);
-    return RF_EINVAL;
-}
-
 template <int BN, int CG>
 static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStream_t st) {
-    if (p.mt == 2) {
-        if constexpr (BN == 256 && CG == 2) return dispatch_mt2<BN, CG>(p, epi, e, st);
-        set_error("gemm: two m-subtiles need 256-wide pair tiles");
-        return RF_EINVAL;
-    }
     switch (epi) {
         case gemm::kStoreBF16: return launch<BN, gemm::kStoreBF16, CG>(p, e, st);
         case gemm::kStoreF32: return launch<BN, gemm::kStoreF32, CG>(p, e, st);
         case gemm::kResidGate:
             // long K: the main loop hides a two-pass residual epilogue; keep the operand stages
-            if (BN == 128 && (p.K >= 4096 || resid_two_pass())) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
-            return launch<BN, gemm::kResidGate, CG>(p, e, st);
+            // (256-wide tiles always stage 64 columns per pass)
+            if constexpr (BN == 256) {
+                return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
+            } else {
+                if (p.K >= 4096 || resid_two_pass()) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
+                return launch<BN, gemm::kResidGate, CG>(p, e, st);
+            }
         case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG>(p, e, st);
         case gemm::kStoreF32Scale: return launch<BN, gemm::kStoreF32Scale, CG>(p, e, st);
         case gemm::kBF16Rope: return launch<BN, gemm::kBF16Rope, CG>(p, e, st);
@@ -130,15 +118,38 @@ static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStre
     return RF_EINVAL;
 }
 
+// Stream-K partial tiles: one [128 rows][256] fp32 slot per CTA of the persistent grid plus
+// one flag per (CTA, epilogue warp).  Shared by every stream-K GEMM of the process: GEMMs
+// using it must not run concurrently on different streams (the DiT forward is one stream).
+static float *g_sk_ws = nullptr;
+static unsigned *g_sk_flags = nullptr;
+
+static int sk_workspace() {
+    if (g_sk_ws) return RF_OK;
+    const size_t n = (size_t)sm_count();
+    RF_TRY_CUDA(cudaMalloc(&g_sk_ws, n * 128 * 256 * sizeof(float)));
+    RF_TRY_CUDA(cudaMalloc(&g_sk_flags, n * 4 * sizeof(unsigned)));
+    RF_TRY_CUDA(cudaMemset(g_sk_flags, 0, n * 4 * sizeof(unsigned)));
+    RF_TRY_CUDA(cudaDeviceSynchronize());
+    return RF_OK;
+}
+
 int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, int64_t K, int64_t lda,
-              int64_t ldb, int bn, int cg, int mt) {
-    if (K % gemm::BK || (bn != 128 && bn != 256) || (cg != 1 && cg != 2) || N % bn || M < 1 ||
-        (mt != 1 && !(mt == 2 && bn == 256 && cg == 2))) {
-        set_error("gemm: unsupported shape M=%lld N=%lld K=%lld BN=%d CG=%d MT=%d", (long long)M, (long long)N,
-                  (long long)K, bn, cg, mt);
+              int64_t ldb, int bn, int cg, int sk) {
+    if (K % gemm::BK || (bn != 128 && bn != 256) || (cg != 1 && cg != 2) || N % bn || M < 1) {
+        set_error("gemm: unsupported shape M=%lld N=%lld K=%lld BN=%d CG=%d", (long long)M, (long long)N,
+                  (long long)K, bn, cg);
         return RF_EINVAL;
     }
-    p->mt = mt;
+    // stream-K when the plan's tiles cover every unit at least once (a split tile then
+    // spans exactly two units); the partial-tile workspace is allocated here, never
+    // inside a graph capture
+    p->sk_num_m = (int)((M + gemm::BM * cg - 1) / (gemm::BM * cg));
+    p->sk = sk && (int64_t)p->sk_num_m * (N / bn) >= sm_count() / cg;
+    if (p->sk) {
+        int rc = sk_workspace();
+        if (rc) return rc;
+    }
     p->M = M;
     p->N = N;
     p->K = K;
@@ -173,12 +184,12 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
     // The tensor maps cover the plan's (maximum) M; a smaller M only shortens the tile walk.
     GemmPlan p = plan;
     if (M > 0 && M < p.M) p.M = M;
-    if (epi == gemm::kResidGate && p.bn == 128 && (p.c_ptr != out || p.c_ld != ldo || p.c_rows != p.M)) {
+    if (epi == gemm::kResidGate && (p.c_ptr != out || p.c_ld != ldo || p.c_rows != p.M)) {
         // the TMA-staged residual epilogue needs a map over `out` (cached when planned)
         int rc = gemm_plan_c(&p, out, ldo);
         if (rc) return rc;
     }
-    if (epi == gemm::kSwiGLU && p.bn == 256 && p.mt == 1 && (p.c_ptr != out || p.c_ld != ldo || p.c_rows != p.M)) {
+    if (epi == gemm::kSwiGLU && p.bn == 256 && (p.c_ptr != out || p.c_ld != ldo || p.c_rows != p.M)) {
         // the TMA-stored SwiGLU epilogue needs a map over `out` (cached when planned)
         int rc = gemm_plan_o(&p, out, ldo);
         if (rc) return rc;
@@ -187,8 +198,8 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
                     vt ? (__nv_bfloat16 *)vt->ptr : nullptr, vt ? vt->col0 : 0, vt ? vt->heads : 0,
                     vt ? vt->ld : 0, vt ? vt->period : 0, vt ? vt->layer_stride : 0, g_trace};
     if (nf) {
-        if ((nf->aux && !(epi == gemm::kResidGate && p.bn == 128)) || (nf->rs_part && epi != gemm::kStoreBF16 && epi != gemm::kCrossAttn)) {
-            set_error("gemm: fused norm needs a BN=128 gated-residual producer / bf16-store consumer");
+        if ((nf->aux && epi != gemm::kResidGate) || (nf->rs_part && epi != gemm::kStoreBF16 && epi != gemm::kCrossAttn)) {
+            set_error("gemm: fused norm needs a gated-residual producer / bf16-store consumer");
             return RF_EINVAL;
         }
         e.aux = (__nv_bfloat16 *)nf->aux;
@@ -218,6 +229,11 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
         e.x_scale = 1.4426950408889634f / sqrtf(128.f);
         return launch<128, gemm::kCrossAttn, 1>(p, e, st);
     }
+    if (p.sk) {
+        e.sk_ws = g_sk_ws;
+        e.sk_flags = g_sk_flags;
+        e.sk_num_m = p.sk_num_m;
+    }
     if (p.bn == 256) return p.cg == 2 ? dispatch<256, 2>(p, epi, e, st) : dispatch<256, 1>(p, epi, e, st);
     return p.cg == 2 ? dispatch<128, 2>(p, epi, e, st) : dispatch<128, 1>(p, epi, e, st);
 }
@@ -235,15 +251,14 @@ extern "C" int rf_gemm_bf16(const void *A, const void *B, void *out, int64_t M, 
                             int64_t gate_ld, int32_t rows_per_batch, float alpha, int32_t block_n,
                             void *stream) {
     // block_n: 128 / 256 = one CTA per 128 x block_n tile; -128 / -256 = a CTA pair
-    // (cta_group::2) per 256 x |block_n| tile; -(256 + 4096) = a CTA pair per 512 x 256 tile
-    // (two m-subtiles per CTA)
+    // (cta_group::2) per 256 x |block_n| tile; + 4096 on |block_n|: stream-K tile walk
     if (!A || !B || !out || (epilogue == gemm::kResidGate && !gate) || epilogue == gemm::kBF16Rope) {
         set_error("rf_gemm_bf16: null argument");
         return RF_EINVAL;
     }
     GemmPlan p;
     const int mag = block_n < 0 ? -block_n : block_n;
-    int rc = gemm_plan(&p, A, B, M, N, K, lda, ldb, mag & 4095, block_n < 0 ? 2 : 1, 1 + (mag >> 12));
+    int rc = gemm_plan(&p, A, B, M, N, K, lda, ldb, mag & 4095, block_n < 0 ? 2 : 1, (mag >> 12) & 1);
     if (rc) return rc;
     return gemm_run(p, epilogue, out, ldo, gate, gate_ld, rows_per_batch, alpha, (cudaStream_t)stream);
 }

@@ -54,9 +54,9 @@ struct EpiArgs {
     unsigned long long *trace;
     // RMSNorm fused across a GEMM boundary (the norm without modulation before the
     // cross-attention query projection):
-    //  kResidGate (TMA-staged, BN = 128): with aux set, also aux[m * aux_ld + n] = bf16 of the
-    //    updated residual and sq_part[(n / 128) * sq_ld + m] = its sum of squares over the
-    //    tile's 128 columns (ascending column order);
+    //  kResidGate (TMA-staged): with aux set, also aux[m * aux_ld + n] = bf16 of the
+    //    updated residual and sq_part[(n / BN) * sq_ld + m] = its sum of squares over the
+    //    tile's BN columns (ascending column order);
     //  kStoreBF16: with rs_part set, acc is scaled by rsqrt(sum_t rs_part[t * rs_ld + m] *
     //    rs_inv_d + rs_eps) (t ascending) before rounding -- the consumer applies the norm.
     __nv_bfloat16 *aux;
@@ -72,6 +72,11 @@ struct EpiArgs {
     // the attention kernel's maps); query head = n / 128, KV head = head / x_group.
     int x_rpb, x_mtpb, x_batches, x_nk, x_group, x_hkv;
     float x_scale;   // log2(e) / sqrt(head dim)
+    // stream-K (null: static tile walk): [units * CG * 128 * BN] fp32 partial tiles and
+    // [units * CG * 4] flags (zero between launches); sk_num_m = the plan's m-tile count
+    float *sk_ws;
+    unsigned *sk_flags;
+    int sk_num_m;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -104,31 +109,67 @@ constexpr int BM = 128, BK = 64;
 // CC: residual columns staged per pass (BN: one pass per tile; 64: two passes, half the
 // staging memory, two more operand stages -- for long K, where the main loop hides the
 // epilogue anyway and latency tolerance matters more).
-template <int BN, int CG = 1, int EPI = 0, int CC = BN, int MT = 1>
+template <int BN, int CG = 1, int EPI = 0, int CC = BN>
 struct Cfg {
     static constexpr int BN_LOAD = BN / CG;   // B rows staged by each CTA
-    static constexpr uint32_t A_BYTES = BM * BK * 2;   // one m-subtile of A per CTA
+    static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN_LOAD * BK * 2;
-    static constexpr uint32_t STAGE_BYTES = MT * A_BYTES + B_BYTES;
-    static constexpr bool TMA_C = EPI == 2 && BN == 128;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr bool TMA_C = EPI == 2;
     static constexpr bool XATT = EPI == 6;   // Q, K, V^T staging (32 KB each) for the epilogue attention
     // TMA_O (SwiGLU, BN = 256): each epilogue warp stages its [32 rows][128 cols] bf16 output
     // in shared memory (two SWIZZLE_128B boxes of 64 columns) and writes it with TMA stores:
     // full-line writes instead of one 16-byte store per row per thread
-    static constexpr bool TMA_O = EPI == 3 && BN == 256 && MT == 1;
+    static constexpr bool TMA_O = EPI == 3 && BN == 256;
     static constexpr int C_COLS = CC;                                           // staged per pass
     static constexpr uint32_t C_WARP_BYTES = TMA_C ? 32u * C_COLS * 4u : (TMA_O ? 32u * 128u * 2u : 0u);
-    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + (TMA_C ? 4u * 1024u : 0u) + (XATT ? 3u * 32768u : 0u);
+    static constexpr uint32_t GATE_WARP_BYTES = TMA_C ? 2u * BN * 4u : 0u;   // the two gate rows a warp can touch
+    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + 4 * GATE_WARP_BYTES + (XATT ? 3u * 32768u : 0u);
     // as many operand stages as fit next to the epilogue staging (227 KB opt-in limit)
     static constexpr uint32_t BUDGET = 232448u - 1024u - 512u - C_BYTES;
     static constexpr int STAGES = (int)(BUDGET / STAGE_BYTES) > 10 ? 10 : (int)(BUDGET / STAGE_BYTES);
     static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + C_BYTES + 512;
-    // TMEM: MT m-subtiles x BN columns per accumulator; two accumulators when they fit
-    // (the epilogue of tile i overlaps the main loop of tile i+1), else one whose halves
-    // are released separately (see the MMA warp).
-    static constexpr int ACC_COLS = MT * BN;
-    static constexpr int NACC = 2 * ACC_COLS <= 512 ? 2 : 1;
 };
+
+// stream-K partial tiles (see walk_init in the kernel): raw fp32 accumulator rows parked in
+// global memory by the unit that computes a split tile's tail k blocks, one flag per
+// (unit, CTA, epilogue warp), consumed (and reset) by the unit that finishes the tile.
+// Layout per epilogue warp: [chunk][8 float4][32 lanes], so every warp-wide access is one
+// contiguous 512-byte run (a row-per-thread layout made these scattered 16-byte accesses).
+__device__ __forceinline__ void sk_store32(float *warp_slot, int chunk, int lane, const uint32_t (&r)[32]) {
+    float4 *dst = (float4 *)warp_slot + chunk * 256 + lane;
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+        __stcg(dst + v * 32, make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                         __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
+}
+__device__ __forceinline__ void sk_add32(const float *warp_slot, int chunk, int lane, uint32_t (&r)[32]) {
+    const float4 *src = (const float4 *)warp_slot + chunk * 256 + lane;
+    float4 pv[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) pv[v] = __ldcg(src + v * 32);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+        const float4 p = pv[v];
+        r[4 * v] = __float_as_uint(__uint_as_float(r[4 * v]) + p.x);
+        r[4 * v + 1] = __float_as_uint(__uint_as_float(r[4 * v + 1]) + p.y);
+        r[4 * v + 2] = __float_as_uint(__uint_as_float(r[4 * v + 2]) + p.z);
+        r[4 * v + 3] = __float_as_uint(__uint_as_float(r[4 * v + 3]) + p.w);
+    }
+}
+__device__ __forceinline__ void sk_set_flag(unsigned *flag, int lane) {
+    __threadfence();   // this lane's partial stores, then the warp, then the release
+    __syncwarp();
+    if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+}
+__device__ __forceinline__ void sk_wait_flag(const unsigned *flag) {
+    unsigned v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v) break;
+        __nanosleep(100);
+    }
+}
 
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -136,20 +177,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *(uint32_t *)&h;
 }
 
-template <int BN, int EPI, int CG = 1, int CC = BN, int MT = 1>
+template <int BN, int EPI, int CG = 1, int CC = BN>
 __global__ void __launch_bounds__(192, 1)
 rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_k,
                const __grid_constant__ CUtensorMap tma_vt, int M, int N, int K, EpiArgs epi) {
     using namespace rf::sm100;
-    using C = Cfg<BN, CG, EPI, CC, MT>;
-    constexpr int TM = BM * CG;   // output rows per m-subtile (per CTA pair when CG = 2)
-    constexpr int ACC_COLS = C::ACC_COLS, NACC = C::NACC;
+    using C = Cfg<BN, CG, EPI, CC>;
+    constexpr int TM = BM * CG;   // output rows per tile (per CTA pair when CG = 2)
     constexpr int STAGES = C::STAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sA = base;
-    uint8_t *sB = base + STAGES * MT * C::A_BYTES;   // A: [stage][m-subtile]
+    uint8_t *sB = base + STAGES * C::A_BYTES;
     uint8_t *sC = sB + STAGES * C::B_BYTES;   // C_BYTES (1024-aligned: stage sizes are multiples of 1 KB)
     uint64_t *full = (uint64_t *)(sC + C::C_BYTES);
     uint64_t *empty = full + STAGES;
@@ -159,8 +199,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     uint64_t *xbar = cfull + 4;              // [3] kCrossAttn: K/V loaded, S done, O done
     uint32_t *tmem_slot = (uint32_t *)(xbar + 3);
     static_assert(!C::XATT || (CG == 1 && BN == 128), "cross-attention epilogue: single-CTA 128-wide tiles");
-    static_assert(MT == 1 || (!C::TMA_C && !C::XATT), "two m-subtiles: register epilogues only");
-    constexpr uint32_t TMEM_COLS = C::XATT ? 512 : NACC * ACC_COLS;   // + S and O of the epilogue attention
+    constexpr uint32_t TMEM_COLS = C::XATT ? 512 : 2 * BN;   // + S and O of the epilogue attention
 
     RF_GTRACE(15);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -202,41 +241,72 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     pdl_launch();
     RF_GTRACE(13);
 
-    const int num_m = C::XATT ? epi.x_batches * epi.x_mtpb : (M + TM * MT - 1) / (TM * MT), num_n = N / BN,
+    // Stream-K (epi.sk_ws set): the tile grid is the PLAN's (epi.sk_num_m m-tiles, fixed
+    // for a given GEMM whatever rows this call has), and unit u owns the contiguous k-block
+    // range [u * total / units, (u + 1) * total / units) of the tile-major k-block sequence,
+    // so every unit does the same MMA work (no partial last wave).  A tile split between
+    // two units: the later unit computes its tail k blocks first and parks the fp32 partial
+    // in sk_ws[unit]; the earlier unit, which reaches the tile's head k blocks last, adds
+    // it (head + tail, a fixed order) and runs the real epilogue.  Split points depend only
+    // on the plan, so a row's result does not depend on how many rows the call has.
+    const bool sk = !C::XATT && epi.sk_ws != nullptr;
+    const int num_m = C::XATT ? epi.x_batches * epi.x_mtpb : sk ? epi.sk_num_m : (M + TM - 1) / TM, num_n = N / BN,
               kblocks = K / BK;
-    // first row of m-subtile j of tile t (kCrossAttn: tiles never straddle two batch entries)
-    auto row0 = [&](int t, int j = 0) {
+    // first row of tile t (kCrossAttn: tiles never straddle two batch entries)
+    auto row0 = [&](int t) {
         const int mt = t % num_m;
         if constexpr (C::XATT) return (mt / epi.x_mtpb) * epi.x_rpb + (mt % epi.x_mtpb) * BM;
-        return (mt * MT + j) * TM + (int)rank * BM;
+        return mt * TM + (int)rank * BM;
     };
     const int num_tiles = num_m * num_n;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile walker id
     const int units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int64_t sk_total = (int64_t)num_tiles * kblocks;
+    // segment walker: every role walks the same (tile, k-block range) sequence
+    struct Walk {
+        int64_t pos, end;
+    };
+    auto walk_init = [&]() -> Walk {
+        if (sk) return Walk{(int64_t)unit * sk_total / units, (int64_t)(unit + 1) * sk_total / units};
+        return Walk{unit, num_tiles};
+    };
+    auto walk_next = [&](Walk &w, int &tile, int &kb0, int &kb1) -> bool {
+        for (;;) {
+            if (w.pos >= w.end) return false;
+            if (sk) {
+                tile = (int)(w.pos / kblocks);
+                kb0 = (int)(w.pos % kblocks);
+                kb1 = (int)min((int64_t)kblocks, kb0 + (w.end - w.pos));
+                w.pos += kb1 - kb0;
+            } else {
+                tile = (int)w.pos;
+                kb0 = 0;
+                kb1 = kblocks;
+                w.pos += units;
+            }
+            if (C::XATT || (tile % num_m) * TM < M) return true;   // else: rows beyond this call's M
+        }
+    };
 
     if (warp == 0) {
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            int it = 0;
-            for (int t = unit; t < num_tiles; t += units, ++it) {
-                const int n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
+            int it = 0, t, kb0, kb1;
+            for (Walk w = walk_init(); walk_next(w, t, kb0, kb1); ++it) {
+                const int m0 = row0(t), n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
                 RF_TRACE(it, 6);
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if constexpr (CG == 2) {
                         // both CTAs' bytes complete on the leader's full barrier
                         if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
                         const uint32_t fb = mapa_shared(&full[stage], 0);
-#pragma unroll
-                        for (int j = 0; j < MT; ++j)
-                            tma_load_2d_pair(sA + (stage * MT + j) * C::A_BYTES, &tma_a, fb, kb * BK, row0(t, j));
+                        tma_load_2d_pair(sA + stage * C::A_BYTES, &tma_a, fb, kb * BK, m0);
                         tma_load_2d_pair(sB + stage * C::B_BYTES, &tma_b, fb, kb * BK, n0);
                     } else {
                         mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-#pragma unroll
-                        for (int j = 0; j < MT; ++j)
-                            tma_load_2d(sA + (stage * MT + j) * C::A_BYTES, &tma_a, &full[stage], kb * BK, row0(t, j));
+                        tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * BK, m0);
                         tma_load_2d(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0);
                     }
                     if (++stage == STAGES) {
@@ -251,80 +321,43 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             constexpr uint32_t idesc = idesc_bf16(TM, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            int it = 0;
-            // MMAs of one k block into m-subtile j's accumulator columns
-            auto issue = [&](int stg, int kb, int j) {
-                const uint32_t d_tmem = tmem + acc * ACC_COLS + j * BN;
-                const uint64_t ad = sdesc_sw128(sA + (stg * MT + j) * C::A_BYTES);
-                const uint64_t bd = sdesc_sw128(sB + stg * C::B_BYTES);
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    if constexpr (CG == 2)
-                        umma_bf16_pair(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | k) != 0);
-                    else
-                        umma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc, (kb | k) != 0);
-                }
-            };
-            auto release = [&](int stg) {
-                if constexpr (CG == 2)
-                    umma_commit_pair(&empty[stg]);
-                else
-                    umma_commit(&empty[stg]);
-            };
-            auto advance = [](int &stg, uint32_t &ph) {
-                if (++stg == STAGES) {
-                    stg = 0;
-                    ph ^= 1;
-                }
-            };
-            for (int t = unit; t < num_tiles; t += units, ++it) {
+            int it = 0, t, kb0, kb1;
+            for (Walk w = walk_init(); walk_next(w, t, kb0, kb1); ++it) {
                 RF_TRACE(it, 0);
-                int kb0 = 0;
-                if constexpr (NACC == 1 && MT == 2) {
-                    // One accumulator: the epilogue releases m-subtile 0's columns first.  Run
-                    // subtile 0's MMAs over the first `lag` k blocks while subtile 1 drains,
-                    // then catch subtile 1 up on the same (still resident) stages.
-                    const int lag = kblocks < STAGES ? kblocks : STAGES;
-                    mbar_wait(&tempty[0], acc_phase ^ 1);
-                    tc_fence_after();
-                    RF_TRACE(it, 1);
-                    int s2 = stage;
-                    uint32_t p2 = phase;
-                    for (int kb = 0; kb < lag; ++kb) {
-                        mbar_wait(&full[s2], p2);
-                        tc_fence_after();
-                        if (kb == 0) RF_TRACE(it, 2);
-                        issue(s2, kb, 0);
-                        advance(s2, p2);
-                    }
-                    mbar_wait(&tempty[1], acc_phase ^ 1);
-                    tc_fence_after();
-                    for (int kb = 0; kb < lag; ++kb) {
-                        issue(stage, kb, 1);
-                        release(stage);
-                        advance(stage, phase);
-                    }
-                    kb0 = lag;
-                } else {
-                    mbar_wait(&tempty[acc], acc_phase ^ 1);
-                    tc_fence_after();
-                    RF_TRACE(it, 1);
-                }
-                for (int kb = kb0; kb < kblocks; ++kb) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                RF_TRACE(it, 1);
+                const uint32_t d_tmem = tmem + acc * BN;
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    if (kb == 0) RF_TRACE(it, 2);
+                    if (kb == kb0) RF_TRACE(it, 2);
+                    const uint64_t ad = sdesc_sw128(sA + stage * C::A_BYTES);
+                    const uint64_t bd = sdesc_sw128(sB + stage * C::B_BYTES);
 #pragma unroll
-                    for (int j = 0; j < MT; ++j) issue(stage, kb, j);
-                    release(stage);
-                    advance(stage, phase);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        if constexpr (CG == 2)
+                            umma_bf16_pair(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                                           (kb != kb0) || k != 0);
+                        else
+                            umma_bf16(d_tmem, ad + (uint64_t)(k * 2), bd + (uint64_t)(k * 2), idesc,
+                                      (kb != kb0) || k != 0);
+                    }
+                    if constexpr (CG == 2)
+                        umma_commit_pair(&empty[stage]);
+                    else
+                        umma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
                 RF_TRACE(it, 3);
                 if constexpr (CG == 2)
                     umma_commit_pair(&tfull[acc]);
                 else
                     umma_commit(&tfull[acc]);
-                if (++acc == NACC) {
+                if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
@@ -340,9 +373,9 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         // ready, and the accumulator is released before the last store.
         const int q = warp & 3;
         uint8_t *sw = sC + q * C::C_WARP_BYTES;   // NB boxes of [32 rows][32 fp32], SWIZZLE_128B
-        float *gs = (float *)(sC + 4 * C::C_WARP_BYTES + q * 1024);   // [2][BN] gate rows
+        float *gs = (float *)(sC + 4 * C::C_WARP_BYTES + q * C::GATE_WARP_BYTES);   // [2][BN] gate rows
         constexpr int NB = CC / 32, NP = BN / CC;
-        static_assert(BN == 128 && NB * 32 * NP == BN, "residual epilogue shape");
+        static_assert((BN == 128 || BN == 256) && NB * 32 * NP == BN, "residual epilogue shape");
         auto tile_m0 = [&](int t) { return (t % num_m) * TM + (int)rank * BM + q * 32; };
         auto tile_n0 = [&](int t) { return (t / num_m) * BN; };
         auto load_pass = [&](int t, int p) {
@@ -351,21 +384,56 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             for (int j = 0; j < NB; ++j)
                 tma_load_2d(sw + j * 4096, &tma_c, &cfull[q], tile_n0(t) + p * CC + j * 32, tile_m0(t));
         };
-        int acc = 0, it = 0;
+        int acc = 0, it = 0, t, kb0, kb1;
         uint32_t acc_phase = 0, c_phase = 0;
-        if (lane == 0 && unit < num_tiles) load_pass(unit, 0);
-        for (int t = unit; t < num_tiles; t += units, ++it) {
+        Walk w = walk_init();
+        bool have = walk_next(w, t, kb0, kb1);
+        // a stream-K tail segment only parks its partial: no residual slice to stage
+        if (lane == 0 && have && !(sk && kb0 > 0)) load_pass(t, 0);
+        while (have) {
+            Walk wn = w;
+            int tn, nk0, nk1;
+            const bool next = walk_next(wn, tn, nk0, nk1);
+            const bool next_load = next && !(sk && nk0 > 0);
             const int m0 = tile_m0(t), n0 = tile_n0(t);
+            const bool sk_put = sk && kb0 > 0, sk_get = sk && kb0 == 0 && kb1 < kblocks;
+            float *sk_slot = sk ? epi.sk_ws + ((size_t)((sk_put ? unit : unit + 1) * CG + rank) * 4 + q) * 32 * BN
+                                : nullptr;
+            if (sk_put) {   // tail k blocks of a split tile: park the raw partial sums
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
+                    tmem_ld_wait();
+                    sk_store32(sk_slot, c0 / 32, lane, r);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2)
+                        mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+                    else
+                        mbar_arrive(&tempty[acc]);
+                }
+                sk_set_flag(epi.sk_flags + (unit * CG + rank) * 4 + q, lane);
+                if (lane == 0 && next_load) load_pass(tn, 0);
+            } else {
             const int m = min(m0 + lane, M - 1);
             const int b_lo = min(m0, M - 1) / epi.rows_per_batch, b_hi = min(m0 + 31, M - 1) / epi.rows_per_batch;
             __syncwarp();   // the previous tile's gate reads are done
-            ((float4 *)gs)[lane] = __ldg((const float4 *)(epi.gate + (int64_t)b_lo * epi.gate_ld + n0) + lane);
-            ((float4 *)gs)[32 + lane] = __ldg((const float4 *)(epi.gate + (int64_t)b_hi * epi.gate_ld + n0) + lane);
+#pragma unroll
+            for (int i = lane; i < BN / 4; i += 32) {
+                ((float4 *)gs)[i] = __ldg((const float4 *)(epi.gate + (int64_t)b_lo * epi.gate_ld + n0) + i);
+                ((float4 *)gs)[BN / 4 + i] = __ldg((const float4 *)(epi.gate + (int64_t)b_hi * epi.gate_ld + n0) + i);
+            }
             __syncwarp();
             const float *gr = gs + (m / epi.rows_per_batch != b_lo ? BN : 0);
             const bool live = m0 + lane < M;
             float ss = 0.f;
             uint2 aux4[8];
+            if (sk_get) sk_wait_flag(epi.sk_flags + ((unit + 1) * CG + rank) * 4 + q);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
@@ -379,6 +447,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     uint32_t r[32];
                     tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col), r);
                     tmem_ld_wait();
+                    if (sk_get) sk_add32(sk_slot, col / 32, lane, r);   // head + tail
                     float4 *row = (float4 *)(sw + j * 4096 + lane * 128);
                     const float4 *gv = (const float4 *)(gr + col);
 #pragma unroll
@@ -419,21 +488,29 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     for (int j = 0; j < NB; ++j) tma_store_2d(&tma_c, sw + j * 4096, n0 + p * CC + j * 32, m0);
                     bulk_commit();
                     if (p == NP - 1 && q == 2) RF_TRACE(it, 5);
-                    const bool more = p + 1 < NP || t + units < num_tiles;
+                    const bool more = p + 1 < NP || next_load;
                     if (more) {
                         bulk_wait_read0();   // the store has read the slice: the buffer is free
                         if (p + 1 < NP)
                             load_pass(t, p + 1);
                         else
-                            load_pass(t + units, 0);
+                            load_pass(tn, 0);
                     }
                 }
             }
             if (epi.aux && live) epi.sq_part[(int64_t)(n0 / BN) * epi.sq_ld + m0 + lane] = ss;
+            if (sk_get && lane == 0) epi.sk_flags[((unit + 1) * CG + rank) * 4 + q] = 0u;   // for the next launch
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
+            w = wn;
+            t = tn;
+            kb0 = nk0;
+            kb1 = nk1;
+            have = next;
+            ++it;
         }
         if (lane == 0) bulk_wait0();
     } else if constexpr (C::XATT) {
@@ -590,16 +667,20 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         }
     } else {
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        int acc = 0, it = 0;
+        int acc = 0, it = 0, t, kb0, kb1;
         uint32_t acc_phase = 0;
-        for (int t = unit; t < num_tiles; t += units, ++it) {
+        for (Walk w = walk_init(); walk_next(w, t, kb0, kb1); ++it) {
             const int n0 = (t / num_m) * BN;
+            // stream-K roles of this segment (see walk_init): park the tail partial / add it
+            const bool sk_put = sk && kb0 > 0, sk_get = sk && kb0 == 0 && kb1 < kblocks;
+            float *sk_slot = sk ? epi.sk_ws + ((size_t)((sk_put ? unit : unit + 1) * CG + rank) * 4 + q) * 32 * BN
+                                : nullptr;
+            if (sk_get) sk_wait_flag(epi.sk_flags + ((unit + 1) * CG + rank) * 4 + q);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
-#pragma unroll 1
-          for (int j = 0; j < MT; ++j) {
-            const int m0 = row0(t, j);
+            {
+            const int m0 = row0(t);
             const int m = m0 + q * 32 + lane;
             const bool live = m < M;
             float rs = 1.0f;   // fused RMSNorm of the A rows (kStoreBF16 with rs_part)
@@ -648,8 +729,13 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                 }
                 uint32_t r[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * ACC_COLS + j * BN + c0), r);
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
                 tmem_ld_wait();
+                if (sk_put) {   // tail k blocks of a split tile: park the raw partial sums
+                    sk_store32(sk_slot, c0 / 32, lane, r);
+                    continue;
+                }
+                if (sk_get) sk_add32(sk_slot, c0 / 32, lane, r);   // head + tail
                 if (!live) continue;
                 const int n = n0 + c0;
                 if constexpr (EPI == kStoreBF16) {
@@ -760,28 +846,18 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                 }
             }
-            if constexpr (NACC == 1) {   // one accumulator: release m-subtile j's columns now
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if constexpr (CG == 2)
-                        mbar_arrive_cluster(mapa_shared(&tempty[j], 0));
-                    else
-                        mbar_arrive(&tempty[j]);
-                }
             }
-          }
-            if constexpr (NACC == 2) {
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if constexpr (CG == 2)
-                        mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
-                    else
-                        mbar_arrive(&tempty[acc]);
-                }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 2)
+                    mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+                else
+                    mbar_arrive(&tempty[acc]);
             }
-            if constexpr (C::TMA_O) {   // rows >= M are clipped by the tensor map
+            if (sk_put) sk_set_flag(epi.sk_flags + (unit * CG + rank) * 4 + q, lane);
+            if (sk_get && lane == 0) epi.sk_flags[((unit + 1) * CG + rank) * 4 + q] = 0u;   // for the next launch
+            if (C::TMA_O && !sk_put) {   // rows >= M are clipped by the tensor map
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -792,7 +868,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 }
             }
             if (q == 2 && lane == 0) RF_TRACE(it, 5);
-            if (++acc == NACC) {
+            if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }

@@ -41,15 +41,16 @@ def test_gemm_bf16_and_scale(ops):
     assert torch.allclose(s, 0.25 * r, rtol=1e-5, atol=1e-3)
 
 
+@pytest.mark.parametrize("bn", [128, 256])
 @pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("B,T,K,N", [(3, 100, 256, 512), (4, 750, 2048, 2048), (1, 77, 128, 256)])
-def test_gemm_resid_gate(ops, pair, B, T, K, N):
+def test_gemm_resid_gate(ops, pair, B, T, K, N, bn):
     a = torch.randn(B * T, K, device="cuda").bfloat16()
     b = torch.randn(N, K, device="cuda").bfloat16()
     gate = torch.randn(B, N, device="cuda")
     x0 = torch.randn(B * T, N, device="cuda")
     x = x0.clone()
-    ops.gemm(a, b, out=x, epilogue=ops.EPI_RESID_GATE, gate=gate, rows_per_batch=T, block_n=128, pair=pair)
+    ops.gemm(a, b, out=x, epilogue=ops.EPI_RESID_GATE, gate=gate, rows_per_batch=T, block_n=bn, pair=pair)
     r = x0 + gate.repeat_interleave(T, 0) * ref(a, b)
     assert torch.allclose(x, r, rtol=1e-5, atol=1e-3)
 
@@ -67,27 +68,42 @@ def test_gemm_swiglu(ops, pair):
     assert torch.allclose(out.float(), r, rtol=2e-2, atol=2e-2)
 
 
-@pytest.mark.parametrize("M,N,K", [(3000, 12288, 2048), (3000, 4096, 2048), (100, 256, 64), (700, 512, 128),
-                                   (513, 256, 320), (6000, 2048, 6144), (1, 256, 64)])
-def test_gemm_two_m_subtiles_bit_identical(ops, M, N, K):
-    """512 x 256 pair tiles (two m-subtiles share each weight stage; one TMEM accumulator
-    whose halves are released separately) give the same bits as 256 x 256 pair tiles: each
-    output element is the same K-ordered tcgen05 accumulation."""
-    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+@pytest.mark.parametrize("M,N,K,bn", [(3000, 2048, 2048, 128), (3000, 2048, 6144, 128), (3000, 4096, 2048, 256),
+                                      (6000, 2048, 2048, 128), (2900, 2048, 320, 128), (3000, 12288, 2048, 256)])
+def test_gemm_stream_k_matches_torch_and_repeats(ops, M, N, K, bn):
+    """Stream-K tile walk (equal k-block shares per CTA pair, split tiles combined head +
+    tail through the partial-tile workspace): same accuracy as the static walk, bit-identical
+    from launch to launch (the flags are consumed and reset by every launch)."""
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + K)
     a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     b = torch.randn(N, K, device="cuda", generator=g).bfloat16()
-    base = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=256, pair=True)
-    two = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=256, pair=True, m_subtiles=2)
-    assert torch.equal(base, two)
+    outs = [ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=bn, pair=True, stream_k=True) for _ in range(3)]
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     r = ref(a, b)
-    assert (two - r).abs().max().item() <= 1e-5 * r.abs().max().item()
+    assert (outs[0] - r).abs().max().item() <= 1e-5 * r.abs().max().item()
+    base = ops.gemm(a, b, epilogue=ops.EPI_F32, block_n=bn, pair=True)
+    assert (outs[0] - base).abs().max().item() <= 1e-5 * r.abs().max().item()
 
 
-def test_gemm_two_m_subtiles_swiglu(ops):
+@pytest.mark.parametrize("bn", [128, 256])
+@pytest.mark.parametrize("B,T,K,N", [(4, 750, 2048, 2048), (4, 750, 6144, 2048), (8, 750, 2048, 2048)])
+def test_gemm_stream_k_resid_gate(ops, B, T, K, N, bn):
+    a = torch.randn(B * T, K, device="cuda").bfloat16()
+    b = (torch.randn(N, K, device="cuda") * 0.05).bfloat16()
+    gate = torch.randn(B, N, device="cuda")
+    x0 = torch.randn(B * T, N, device="cuda")
+    x = x0.clone()
+    ops.gemm(a, b, out=x, epilogue=ops.EPI_RESID_GATE, gate=gate, rows_per_batch=T, block_n=bn, pair=True,
+             stream_k=True)
+    r = x0 + gate.repeat_interleave(T, 0) * ref(a, b)
+    assert torch.allclose(x, r, rtol=1e-5, atol=1e-3)
+
+
+def test_gemm_stream_k_swiglu(ops):
     M, K, H = 3000, 2048, 6144
     g = torch.Generator(device="cuda").manual_seed(5)
     a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     w = (torch.randn(2 * H, K, device="cuda", generator=g) * 0.02).bfloat16()
     base = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256, pair=True)
-    two = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256, pair=True, m_subtiles=2)
-    assert torch.equal(base, two)
+    sk = ops.gemm(a, w, epilogue=ops.EPI_SWIGLU, block_n=256, pair=True, stream_k=True)
+    assert (sk.float() - base.float()).abs().max().item() <= 2e-2

@@ -7,7 +7,7 @@ O=gpurun_out/$TAG
 mkdir -p $O
 timeout 400 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_dit.py -x -q > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
 timeout 200 python tools/dit_check.py 4 --graph > $O/dit_check.txt 2>&1
-timeout 200 python tools/gemm_mt_bench.py > $O/gemm_bench.txt 2>&1
+timeout 200 python tools/gemm_sk_bench.py > $O/gemm_bench.txt 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'rf_|gemm' -c 700 --csv \
   --log-file $O/launches.csv python tools/dit_check.py 4 --no-ref > $O/ncu.log 2>&1
 tail -n 2 $O/pytest.log; cat $O/dit_check.txt $O/gemm_bench.txt
