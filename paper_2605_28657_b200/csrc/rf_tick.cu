@@ -155,6 +155,72 @@ __device__ __forceinline__ double group_sum(double v) {
     return v;
 }
 
+// The common row (one condition, no guidance, SDE step, no morph target): the same
+// operations in the same order as velocity_elem + solve_elem, but every operand of a
+// lane's two channels is fetched with one 16-byte (8-byte for fp32 velocities) load,
+// all of them issued before any arithmetic, so a thread makes one memory round trip
+// instead of a chain of dependent scalar loads.  The kernel is HBM-bound; this is what
+// lets it approach the roofline (bench.py toy_path.solver_roofline).
+__device__ __forceinline__ bool fast_row(const rf_row &R, int64_t D) {
+    const uintptr_t al = (uintptr_t)R.x | (uintptr_t)R.cond_x0[0] | (uintptr_t)R.noise_step |
+                         (uintptr_t)R.source | (uintptr_t)R.noise_model;
+    const uintptr_t need = (R.flags & RF_ROWF_V_F32) ? 7 : 15;
+    return R.n_cond == 1 && R.neg_kind == RF_NEG_NONE && R.solver == RF_SOLVER_SDE && !R.x0_target &&
+           !R.v_out && !(R.flags & RF_ROWF_NO_STEP) && R.x && R.noise_step && (D % 2) == 0 &&
+           ((((uintptr_t)R.x | (uintptr_t)R.noise_step | (uintptr_t)R.source | (uintptr_t)R.noise_model) & 15) == 0) &&
+           ((al & need) == 0);
+}
+
+__device__ __forceinline__ double2 ld2(const double *p) { return __ldg((const double2 *)p); }
+
+__device__ __forceinline__ void fast_pair(const rf_row &R, const double *__restrict__ style, int64_t f, int64_t i) {
+    const double2 x = *(const double2 *)(R.x + i);
+    const bool cond_v = (R.flags & RF_ROWF_COND_V) != 0;
+    double2 vg = make_double2(0.0, 0.0), x0p = vg, st = vg, nm = vg, src = vg;
+    if (cond_v) {
+        if (R.flags & RF_ROWF_V_F32) {
+            const float2 v32 = __ldg((const float2 *)R.cond_x0[0] + i / 2);
+            vg = make_double2((double)v32.x, (double)v32.y);
+        } else {
+            vg = ld2(R.cond_x0[0] + i);
+        }
+    } else {
+        x0p = ld2(R.cond_x0[0] + i);
+        st = ld2(style + i);
+        if (R.noise_model) nm = ld2(R.noise_model + i);
+    }
+    const double2 n = ld2(R.noise_step + i);
+    if (R.source) src = ld2(R.source + i);
+    const double c = R.source ? curve_or(R.curves[RF_CURVE_SDE], f, 1.0) : 1.0;
+    const double tc = R.t_curr, tn = R.t_next;
+    const double xv[2] = {x.x, x.y}, vgv[2] = {vg.x, vg.y}, x0v[2] = {x0p.x, x0p.y}, sv[2] = {st.x, st.y},
+                 nmv[2] = {nm.x, nm.y}, nv[2] = {n.x, n.y}, srcv[2] = {src.x, src.y};
+    double out[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        double v;
+        if (cond_v) {
+            v = vgv[e];
+        } else {   // toy_velocity
+            const double x0 = dadd(x0v[e], sv[e]);
+            v = ddiv(dsub(xv[e], x0), tc);
+            if (R.noise_model) v = dadd(v, dmul(R.jitter_t, nmv[e]));
+        }
+        // solve_elem, SDE, no morph
+        const double x0pe = dsub(xv[e], dmul(v, tc));
+        const double tnn = dmul(tn, nv[e]);
+        const double omt = dsub(1.0, tn);
+        const double full = dadd(tnn, dmul(omt, x0pe));
+        if (!R.source) {
+            out[e] = full;
+        } else {
+            const double sr = dadd(tnn, dmul(omt, srcv[e]));
+            out[e] = dadd(dmul(c, full), dmul(dsub(1.0, c), sr));
+        }
+    }
+    *(double2 *)(R.x + i) = make_double2(out[0], out[1]);
+}
+
 template <int LPF>
 __global__ void __launch_bounds__(256)
 rf_tick_kernel(const __grid_constant__ TickBatch B, int64_t T, int64_t D, const double *__restrict__ style) {
@@ -165,6 +231,18 @@ rf_tick_kernel(const __grid_constant__ TickBatch B, int64_t T, int64_t D, const 
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
     const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const bool rescale = R.neg_kind != RF_NEG_NONE && R.curves[RF_CURVE_RESCALE] != nullptr;
+    if (fast_row(R, D)) {
+        for (int64_t f0 = wid * FPW; f0 < T; f0 += warps_total * FPW) {
+            const int64_t f = f0 + sub;
+            if (f >= T) continue;
+#pragma unroll
+            for (int g = 0; g < kTickMaxGroups; ++g) {
+                const int64_t c = (int64_t)g * 2 * LPF + 2 * gl;
+                if (c < D) fast_pair(R, style, f, f * D + c);
+            }
+        }
+        return;
+    }
 
     for (int64_t f0 = wid * FPW; f0 < T; f0 += warps_total * FPW) {
         const int64_t f = f0 + sub;
