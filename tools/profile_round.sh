@@ -1,0 +1,22 @@
+#!/bin/bash
+# Profiles for the round's evidence (profiles/): ncu --set full of the DiT forward's top
+# kernels (one launch each, mid-forward), and the forward's DRAM traffic launch lists
+# (cold: ncu flushes caches before each kernel; warm: --cache-control none).
+# Usage: gpurun --timeout 1500 -- 'bash tools/profile_round.sh TAG'
+TAG=${1:-prof}
+O=gpurun_out/$TAG
+mkdir -p $O
+P='python tools/dit_check.py 4 --no-ref'
+for spec in "gateup:rf_gemm_kernel<\(int\)256, \(int\)3, \(int\)2" "down:rf_gemm_kernel<\(int\)128, \(int\)2, \(int\)2, \(int\)64" \
+            "oproj:rf_gemm_kernel<\(int\)128, \(int\)2, \(int\)2, \(int\)128" "qkv:rf_gemm_kernel<\(int\)256, \(int\)5, \(int\)2" \
+            "xq_xattn:rf_gemm_kernel<\(int\)128, \(int\)6" "attn_self:rf_attn_fa64_kernel" "norm:rf_dit_norm_mod" \
+            "tick_solve:rf_tick_kernel"; do
+  n=${spec%%:*}; r=${spec#*:}
+  if [ $n = tick_solve ]; then prog='python tools/toy_ticks.py 40'; else prog=$P; fi
+  timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k "regex:$r" -s 12 -c 1 -o $O/$n $prog > $O/$n.log 2>&1
+done
+M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:rf_|gemm -c 700 --csv"
+timeout 300 ncu $M --log-file $O/cold.csv $P > /dev/null 2>&1
+timeout 300 ncu $M --cache-control none --log-file $O/warm.csv $P > /dev/null 2>&1
+ls -la $O
