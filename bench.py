@@ -13,8 +13,12 @@ the ring completes one generation every 2 ticks.
   e2e       = the same through the public API with host buffers: per-tick shared-curve
               write from host memory, every CompletionRecord.latent read back to host
   toy_path  = the same ring with the reference's own ToyFlowModel as velocity model (the
-              only model the reference has), for the apples-to-apples CPU comparison
-  cpu_baseline / --impl reference = the reference's CPU path (oracle port, float64 numpy)
+              only model the reference has); compare with cpu_baseline_toy_model
+  cpu_baseline / --impl reference = the same config-2 workload on the host CPU: the
+              reference's tick (oracle port, float64 numpy) with the DiT (oracle/dit_fp32.py,
+              fp32 torch on all host threads) in its model slot; the reference arm also
+              reports the reference's toy model on all cores (`toy_model`)
+  library_baseline = the same DiT forward in stock PyTorch (cuBLAS + SDPA) on the GPU
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -393,7 +397,10 @@ def run_ours(args):
     if library is not None:
         line["library_baseline"] = library
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, processes=1)
+        # the same workload (config 2 with the DiT) on the box's host cores, bounded sample
+        line["cpu_baseline"] = cpu_dit_baseline(args.cpu_seconds, os.cpu_count() or 1)
+        # and the reference's own toy model on one core (its CPU speed on its only model)
+        line["cpu_baseline_toy_model"] = cpu_baseline(args.cpu_seconds, processes=1)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -438,20 +445,64 @@ def cpu_baseline(seconds, processes=1):
                       f"1 thread/process"}
 
 
+def cpu_dit_baseline(seconds, threads, max_ticks=None):
+    """Config 2 on the host CPU: the reference's tick (oracle/ringflow_np.py, float64 numpy)
+    with the DiT in its model slot (oracle/dit_fp32.py: the same network, fp32 torch on all
+    `threads` host threads; one forward per ring row per tick).  The ring is filled with the
+    toy model first (cheap), then steady-state DiT ticks are timed: at least one, then until
+    `seconds` or `max_ticks`.  completions/s = row-steps / S / wall (every completion is S
+    row-steps; at depth 4 one completes every other tick)."""
+    import torch
+
+    import scenarios
+
+    import oracle.ringflow_np as O
+    from oracle.dit_fp32 import CpuDiTVelocity
+    from paper_2605_28657_b200.dit import DiTConfig
+
+    torch.set_num_threads(threads)
+    src = scenarios.keyed(0, "bench-source", (T, D))
+    req = O.Request([O.Cond(O.chash("bench", "bench prompt"), source=src)])
+    pipe = O.Pipeline(depth=DEPTH, steps=STEPS, frames=T, channels=D, seed=0, request=req)
+    for _ in range(4 * STEPS):
+        pipe.tick()
+    pipe.model = CpuDiTVelocity(DiTConfig(), T)
+    pipe.tick()   # untimed: first-touch of the fp32 weights
+    row_steps, ticks = 0, 0
+    t0 = time.perf_counter()
+    while ticks == 0 or (time.perf_counter() - t0 < seconds and (max_ticks is None or ticks < max_ticks)):
+        row_steps += sum(1 for s in pipe.slots if s is not None)
+        pipe.tick()
+        ticks += 1
+    wall = time.perf_counter() - t0
+    return {"value": round(row_steps / STEPS / wall, 5), "unit": UNIT, "cores": threads, "kind": "port",
+            "ticks": ticks,
+            "sample": f"config 2 on the host CPU: oracle/ringflow_np.py tick (the reference's algorithm, float64 "
+                      f"numpy) with the ACE-Step-shape DiT (oracle/dit_fp32.py, fp32 torch, {threads} threads) in "
+                      f"the model slot; {ticks} steady-state tick(s) ({row_steps} DiT row forwards + SDE steps) "
+                      f"in {wall:.1f} s after the ring was filled; completions/s = row-steps / S / wall"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     procs = os.cpu_count() or 1
-    per_step = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
-    base = cpu_baseline(per_step * args.steps, processes=procs)
+    # each step = one steady-state config-2 tick on the CPU; bounded to ~90 s of ticks
+    base = cpu_dit_baseline(90.0, procs, max_ticks=args.steps)
+    toy = cpu_baseline(10.0, processes=procs)
     line = {
         "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": "config 2 shape: 60-s latent T=1500 x D=64, ring depth 4, S=8, toy velocity model "
-                               "(the reference's only model), source present; one stream per host core"},
+        "steps": base["ticks"], "steps_requested": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 DiT / f64 tick", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "config 2: ACE-Step-1.5-shape 24-layer DiT (d=2048, 16/8 heads, SwiGLU 6144, "
+                               "random init), 60-s latent T=1500 x D=64, ring depth 4, S=8, source present, "
+                               "denoise 1.0; the reference's tick on the host CPU (oracle port) with the DiT "
+                               "(fp32 torch, all host threads) in its model slot"},
         "cpu_baseline": base,
+        "toy_model": {**toy, "note": "the reference's own ToyFlowModel at config-2 shape, one stream per host "
+                                     "core: the reference's CPU speed on its only model"},
         "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

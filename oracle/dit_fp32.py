@@ -1,0 +1,147 @@
+"""CPU / fp32 oracle of the DiT velocity model (the ACE-Step-1.5-shape network that fills the
+reference's model slot, ``model.py:91-152``, at BASELINE configs 2-5).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, tools/ and bench.py's CPU baseline / reference arm
+import this module; the product package (paper_2605_28657_b200/) never does.
+
+* ``forward_fp32`` -- the network in plain PyTorch fp32 (bf16 weights upcast, no TF32), with
+  the same bf16 rounding points as the sm_100a forward (csrc/rf_dit.cu).  The reference has
+  no DiT, so DiT parity is unpinned by it; this is the oracle the GPU
+  forward is tested against (tests/test_gpu_dit.py, rel-RMS tolerance stated there).
+* ``reference_forward(dit, ...)`` -- the same on a GPU ``DiT``'s own weights.
+* ``CpuDiTVelocity`` -- the network on the host CPU with fp32 weights, plugged into the
+  oracle pipeline's model slot (``oracle/ringflow_np.py``: ``Pipeline.model.velocity``) so
+  bench.py can time the reference's CPU path at config 2 on the same workload as the GPU
+  arm (a DiT forward per ring row per tick), not the toy model.
+"""
+from __future__ import annotations
+
+import math
+from types import SimpleNamespace
+
+import numpy as np
+import torch
+
+
+def _rmsnorm(x, eps):
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps)
+
+
+def _rope(x, cos, sin):
+    # interleaved pairs (2i, 2i+1) of each 128-dim head; x [B, N, H, 128]
+    x0, x1 = x[..., 0::2], x[..., 1::2]
+    y0 = x0 * cos - x1 * sin
+    y1 = x0 * sin + x1 * cos
+    return torch.stack([y0, y1], -1).flatten(-2)
+
+
+def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float()):
+    """The DiT in fp32.  cfg: DiTConfig; W: weights with the DiTWeights attribute names
+    (f maps a stored weight to the fp32 tensor used); xs: [frames, C] latents; ts: per-row
+    timesteps; conds: [n_cond_tokens, d] conditioning tokens.  Returns [B, frames, C]."""
+    B, T, C = len(xs), frames, cfg.latent_channels
+    N, d = T // cfg.patch, cfg.d_model
+    H, Hk, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+    x = torch.stack([xx.float() for xx in xs]).reshape(B, N, cfg.in_dim)
+    x = x.bfloat16().float()
+    dev = x.device
+    half = cfg.freq_dim // 2
+    freqs = torch.exp(-math.log(10000.0) * torch.arange(half, device=dev, dtype=torch.float32) / half)
+    args = 1000.0 * torch.tensor([float(t) for t in ts], device=dev)[:, None] * freqs[None]
+    tf = torch.cat([torch.cos(args), torch.sin(args)], -1).bfloat16().float()
+    silu = torch.nn.functional.silu
+    temb = silu(tf @ f(W.w_t1).T).bfloat16().float() @ f(W.w_t2).T
+    st = silu(temb).bfloat16().float()
+    mod = st @ f(W.w_ada).T                       # [B, 6d]
+    fmod = st @ f(W.w_final_ada).T                # [B, 2d]
+    h = x @ f(W.w_in).T                           # [B, N, d]
+    pos = torch.arange(N, device=dev, dtype=torch.float64)
+    inv = torch.pow(torch.tensor(cfg.rope_theta, dtype=torch.float64),
+                    -2.0 * torch.arange(64, device=dev, dtype=torch.float64) / 128.0)
+    ang = pos[:, None] * inv[None]
+    cos, sin = torch.cos(ang).float()[None, :, None, :], torch.sin(ang).float()[None, :, None, :]
+    cond = torch.stack([c.float() for c in conds])  # [B, Nc, d]
+    bfr = lambda t: t.bfloat16().float()  # noqa: E731
+    L = cfg.n_layers if layers is None else layers
+    for l in range(L):
+        m = mod + W.ada_table[l][None]
+        sh1, sc1, g1, sh2, sc2, g2 = [m[:, i * d:(i + 1) * d][:, None, :] for i in range(6)]
+        a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc1) + sh1)
+        qkv = bfr(a @ f(W.w_qkv[l]).T)
+        q = qkv[..., :H * hd].reshape(B, N, H, hd)
+        k = qkv[..., H * hd:(H + Hk) * hd].reshape(B, N, Hk, hd)
+        v = qkv[..., (H + Hk) * hd:].reshape(B, N, Hk, hd)
+        q, k = bfr(_rope(q, cos, sin)), bfr(_rope(k, cos, sin))
+        k = k.repeat_interleave(H // Hk, dim=2)
+        v = v.repeat_interleave(H // Hk, dim=2)
+        o = torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                                             v.transpose(1, 2))
+        o = bfr(o.transpose(1, 2).reshape(B, N, H * hd))
+        h = h + g1 * (o @ f(W.w_o[l]).T)
+        c = bfr(_rmsnorm(h, cfg.norm_eps))
+        qc = bfr(c @ f(W.w_qc[l]).T).reshape(B, N, H, hd)
+        kvc = bfr(cond @ f(W.w_kvc[l]).T)
+        kc = kvc[..., :Hk * hd].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
+        vc = kvc[..., Hk * hd:].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
+        oc = torch.nn.functional.scaled_dot_product_attention(qc.transpose(1, 2), kc.transpose(1, 2),
+                                                              vc.transpose(1, 2))
+        oc = bfr(oc.transpose(1, 2).reshape(B, N, H * hd))
+        h = h + oc @ f(W.w_oc[l]).T
+        mm = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc2) + sh2)
+        gu = mm @ f(W.w_gu[l]).T
+        gt, up = bfr(gu[..., 0::2]), bfr(gu[..., 1::2])
+        hid = bfr(silu(gt) * up)
+        h = h + g2 * (hid @ f(W.w_down[l]).T)
+    shf, scf = fmod[:, :d][:, None, :], fmod[:, d:][:, None, :]
+    a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + scf) + shf)
+    v = a @ f(W.w_out).T
+    return v.reshape(B, T, C)
+
+
+def reference_forward(dit, xs, ts, conds, layers: int = None) -> torch.Tensor:
+    """forward_fp32 on a (GPU) ``paper_2605_28657_b200.dit.DiT``'s own bf16 weights, no TF32."""
+    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        return forward_fp32(dit.cfg, dit.weights, dit.frames, xs, ts, conds, layers)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+
+
+class CpuDiTVelocity:
+    """The DiT as the oracle pipeline's model (``velocity(x, t, cond, style, seed, stream,
+    step)`` like ``ringflow_np.Toy``): one fp32 CPU forward per ring row per step, seeded
+    random-init weights of the config's shape (bf16-representable values, kept in fp32)."""
+
+    def __init__(self, cfg, frames: int, seed: int = 1234):
+        self.cfg, self.frames = cfg, frames
+        g = torch.Generator().manual_seed(seed)
+        d, L, F = cfg.d_model, cfg.n_layers, cfg.mlp_hidden
+        q, kv = cfg.n_heads * cfg.head_dim, cfg.n_kv_heads * cfg.head_dim
+
+        def lin(*shape, std=None):
+            s = std if std is not None else 1.0 / math.sqrt(shape[-1])
+            return (torch.randn(*shape, generator=g) * s).bfloat16().float()
+
+        gate, up = lin(L, F, d), lin(L, F, d)
+        self.W = SimpleNamespace(
+            w_in=lin(d, cfg.in_dim), w_t1=lin(d, cfg.freq_dim), w_t2=lin(d, d), w_ada=lin(6 * d, d, std=0.02),
+            ada_table=torch.randn(L, 6 * d, generator=g) * 0.1, w_qkv=lin(L, q + 2 * kv, d), w_o=lin(L, d, q),
+            w_qc=lin(L, q, d), w_kvc=lin(L, 2 * kv, d), w_oc=lin(L, d, q),
+            w_gu=torch.stack([gate, up], dim=2).reshape(L, 2 * F, d).contiguous(), w_down=lin(L, d, F),
+            w_final_ada=lin(2 * d, d, std=0.02), w_out=lin(cfg.in_dim, d))
+        self._cond = {}
+
+    def cond_tokens(self, prompt_hash: int) -> torch.Tensor:
+        t = self._cond.get(prompt_hash)
+        if t is None:
+            g = torch.Generator().manual_seed(int(prompt_hash) & ((1 << 62) - 1))
+            t = torch.randn(self.cfg.n_cond_tokens, self.cfg.d_model, generator=g).bfloat16().float()
+            self._cond[prompt_hash] = t
+        return t
+
+    def velocity(self, x, t, c, style, seed, stream, step):
+        with torch.no_grad():
+            v = forward_fp32(self.cfg, self.W, self.frames, [torch.from_numpy(np.ascontiguousarray(x))], [t],
+                             [self.cond_tokens(c.prompt_hash)], f=lambda w: w)
+        return v[0].double().numpy()

@@ -12,7 +12,7 @@ PAPER.md:44,226,242).  This module defines a builder-chosen model of that shape
 
 The forward is one C-ABI call (``rf_dit_forward``, csrc/rf_dit.cu): tcgen05 GEMMs fed by
 TMA with fused epilogues (RoPE, SwiGLU, AdaLN-gated residual), flash attention, fused
-RMSNorm+modulation.  ``reference_forward`` is the same network in plain PyTorch fp32 --
+RMSNorm+modulation.  ``oracle/dit_fp32.py`` is the same network in plain PyTorch fp32 --
 the oracle the DiT is tested against (DiT parity is unpinned by the reference itself).
 """
 from __future__ import annotations
@@ -201,86 +201,6 @@ class DiT:
         _native.check(self.lib.rf_dit_forward(self.handle, n, xp, tp, cp, out.data_ptr(),
                                               _device.current_stream_handle()), "rf_dit_forward")
         return out[:n]
-
-
-# ---------------------------------------------------------------- fp32 oracle ----
-def _rmsnorm(x, eps):
-    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps)
-
-
-def _rope(x, cos, sin):
-    # interleaved pairs (2i, 2i+1) of each 128-dim head; x [B, N, H, 128]
-    x0, x1 = x[..., 0::2], x[..., 1::2]
-    y0 = x0 * cos - x1 * sin
-    y1 = x0 * sin + x1 * cos
-    return torch.stack([y0, y1], -1).flatten(-2)
-
-
-def reference_forward(dit: DiT, xs, ts, conds, layers: int = None) -> torch.Tensor:
-    """The same network in plain PyTorch fp32 (bf16 weights upcast), no TF32."""
-    cfg, W = dit.cfg, dit.weights
-    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        f = lambda w: w.float()  # noqa: E731
-        B, T, C = len(xs), dit.frames, cfg.latent_channels
-        N, d = T // cfg.patch, cfg.d_model
-        H, Hk, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
-        x = torch.stack([xx.float() for xx in xs]).reshape(B, N, cfg.in_dim)
-        x = x.bfloat16().float()
-        half = cfg.freq_dim // 2
-        freqs = torch.exp(-math.log(10000.0) * torch.arange(half, device=x.device, dtype=torch.float32) / half)
-        args = 1000.0 * torch.tensor([float(t) for t in ts], device=x.device)[:, None] * freqs[None]
-        tf = torch.cat([torch.cos(args), torch.sin(args)], -1).bfloat16().float()
-        silu = torch.nn.functional.silu
-        temb = silu(tf @ f(W.w_t1).T).bfloat16().float() @ f(W.w_t2).T
-        st = silu(temb).bfloat16().float()
-        mod = st @ f(W.w_ada).T                       # [B, 6d]
-        fmod = st @ f(W.w_final_ada).T                # [B, 2d]
-        h = x @ f(W.w_in).T                           # [B, N, d]
-        pos = torch.arange(N, device=x.device, dtype=torch.float64)
-        inv = torch.pow(torch.tensor(cfg.rope_theta, dtype=torch.float64),
-                        -2.0 * torch.arange(64, device=x.device, dtype=torch.float64) / 128.0)
-        ang = pos[:, None] * inv[None]
-        cos, sin = torch.cos(ang).float()[None, :, None, :], torch.sin(ang).float()[None, :, None, :]
-        cond = torch.stack([c.float() for c in conds])  # [B, Nc, d]
-        bfr = lambda t: t.bfloat16().float()  # noqa: E731
-        L = cfg.n_layers if layers is None else layers
-        for l in range(L):
-            m = mod + W.ada_table[l][None]
-            sh1, sc1, g1, sh2, sc2, g2 = [m[:, i * d:(i + 1) * d][:, None, :] for i in range(6)]
-            a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc1) + sh1)
-            qkv = bfr(a @ f(W.w_qkv[l]).T)
-            q = qkv[..., :H * hd].reshape(B, N, H, hd)
-            k = qkv[..., H * hd:(H + Hk) * hd].reshape(B, N, Hk, hd)
-            v = qkv[..., (H + Hk) * hd:].reshape(B, N, Hk, hd)
-            q, k = bfr(_rope(q, cos, sin)), bfr(_rope(k, cos, sin))
-            k = k.repeat_interleave(H // Hk, dim=2)
-            v = v.repeat_interleave(H // Hk, dim=2)
-            o = torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
-                                                                 v.transpose(1, 2))
-            o = bfr(o.transpose(1, 2).reshape(B, N, H * hd))
-            h = h + g1 * (o @ f(W.w_o[l]).T)
-            c = bfr(_rmsnorm(h, cfg.norm_eps))
-            qc = bfr(c @ f(W.w_qc[l]).T).reshape(B, N, H, hd)
-            kvc = bfr(cond @ f(W.w_kvc[l]).T)
-            kc = kvc[..., :Hk * hd].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
-            vc = kvc[..., Hk * hd:].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
-            oc = torch.nn.functional.scaled_dot_product_attention(qc.transpose(1, 2), kc.transpose(1, 2),
-                                                                  vc.transpose(1, 2))
-            oc = bfr(oc.transpose(1, 2).reshape(B, N, H * hd))
-            h = h + oc @ f(W.w_oc[l]).T
-            mm = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc2) + sh2)
-            gu = mm @ f(W.w_gu[l]).T
-            gt, up = bfr(gu[..., 0::2]), bfr(gu[..., 1::2])
-            hid = bfr(silu(gt) * up)
-            h = h + g2 * (hid @ f(W.w_down[l]).T)
-        shf, scf = fmod[:, :d][:, None, :], fmod[:, d:][:, None, :]
-        a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + scf) + shf)
-        v = a @ f(W.w_out).T
-        return v.reshape(B, T, C)
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
 
 
 # ------------------------------------------------- StreamPipeline velocity model --

@@ -1,4 +1,4 @@
-"""DiT velocity model on sm_100a vs its plain-PyTorch fp32 oracle (reference_forward).
+"""DiT velocity model on sm_100a vs its plain-PyTorch fp32 oracle (oracle/dit_fp32.py).
 
 The reference package has no DiT, so DiT parity is against the builder's
 own fp32 forward of the same seeded bf16 weights.  Tolerances are relative RMS errors,
@@ -10,6 +10,8 @@ import math
 import numpy as np
 import pytest
 import torch
+
+from oracle.dit_fp32 import reference_forward
 
 pytestmark = pytest.mark.gpu
 
@@ -132,7 +134,7 @@ def test_small_dit_vs_fp32_oracle(dit_mod):
     dit = dit_mod.DiT(cfg, frames=96, max_rows=4)
     xs, ts, conds = _inputs(dit, 3, 96, 64)
     out = dit.forward(xs, ts, conds).clone()
-    ref = dit_mod.reference_forward(dit, xs, ts, conds)
+    ref = reference_forward(dit, xs, ts, conds)
     assert out.shape == ref.shape and torch.isfinite(out).all()
     assert rel_rms(out, ref) < 1e-2   # 2 layers, d=256
 
@@ -153,7 +155,7 @@ def test_full_size_dit_vs_fp32_oracle(dit_mod):
     dit = dit_mod.DiT(dit_mod.DiTConfig(), frames=1500, max_rows=4)
     xs, ts, conds = _inputs(dit, 4, 1500, 64, seed=1)
     out = dit.forward(xs, ts, conds).clone()
-    ref = dit_mod.reference_forward(dit, xs, ts, conds)
+    ref = reference_forward(dit, xs, ts, conds)
     assert torch.isfinite(out).all()
     assert rel_rms(out, ref) < 3e-2   # 24 layers of bf16 operands
 

@@ -100,3 +100,34 @@ def test_codec_goldens(goldens):
     assert np.array_equal(c64.window(goldens["codec64_latent"], 10, 25, 15), goldens["codec64_win"])
     assert O.quantize(np.array([0.0, 0.5 / 32767, -0.5 / 32767, 1.0, -1.0, 2.0, -2.0])).tolist() == \
         goldens["quantize_kat"].tolist()
+
+
+def test_cpu_dit_velocity_small_config():
+    """oracle/dit_fp32.py (the fp32 DiT the CPU arm and the GPU parity tests use): a row's
+    velocity matches its single-row forward up to bf16 rounding-point flips (the fp32 GEMMs
+    differ in the last bits between batch shapes), and the model plugs into the oracle
+    pipeline's model slot (finite velocities, the ring steps)."""
+    import numpy as np
+    import torch
+
+    import oracle.ringflow_np as O
+    from oracle.dit_fp32 import CpuDiTVelocity, forward_fp32
+    from paper_2605_28657_b200.dit import DiTConfig
+
+    cfg = DiTConfig().small()
+    m = CpuDiTVelocity(cfg, frames=64, seed=3)
+    g = torch.Generator().manual_seed(0)
+    xs = [torch.randn(64, cfg.latent_channels, generator=g, dtype=torch.float64) for _ in range(3)]
+    conds = [m.cond_tokens(i) for i in range(3)]
+    with torch.no_grad():
+        both = forward_fp32(cfg, m.W, 64, xs, [0.9, 0.5, 0.2], conds, f=lambda w: w)
+        one = forward_fp32(cfg, m.W, 64, xs[1:2], [0.5], conds[1:2], f=lambda w: w)
+    rel = ((both[1] - one[0]).pow(2).mean().sqrt() / one[0].pow(2).mean().sqrt()).item()
+    assert rel < 1e-2, rel
+    req = O.Request([O.Cond(O.chash("p", "x"), source=np.zeros((64, cfg.latent_channels)))])
+    pipe = O.Pipeline(depth=2, steps=4, frames=64, channels=cfg.latent_channels, seed=0, request=req)
+    pipe.model = m
+    recs = []
+    for _ in range(8):
+        recs += pipe.tick()
+    assert recs and all(np.isfinite(r.latent).all() for r in recs)

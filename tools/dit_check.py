@@ -6,6 +6,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_28657_b200 import dit as D  # noqa: E402
+from oracle.dit_fp32 import reference_forward  # noqa: E402
 
 
 def main():
@@ -20,7 +21,7 @@ def main():
     conds = [dit.cond_tokens(i) for i in range(rows)]
     out = dit.forward(xs, ts, conds).clone()
     if "--no-ref" not in sys.argv:
-        ref = D.reference_forward(dit, xs, ts, conds)
+        ref = reference_forward(dit, xs, ts, conds)
         err = ((out - ref).pow(2).mean().sqrt() / ref.pow(2).mean().sqrt()).item()
         print(f"rows={rows} rel_rms_vs_fp32={err:.3e} out_rms={out.pow(2).mean().sqrt().item():.3f}")
     for _ in range(3):

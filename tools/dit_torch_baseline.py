@@ -15,6 +15,7 @@ import torch.nn.functional as F
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_28657_b200 import dit as D  # noqa: E402
+from oracle.dit_fp32 import reference_forward  # noqa: E402
 
 
 def build(dit, xs, ts, conds):
@@ -107,7 +108,7 @@ def _compare(rows, n, check):
         if check:
             ours = dit.forward(xs, ts, conds).clone()
             lib = fwd()
-            ref = D.reference_forward(dit, xs, ts, conds)
+            ref = reference_forward(dit, xs, ts, conds)
             rr = lambda a: ((a - ref).pow(2).mean().sqrt() / ref.pow(2).mean().sqrt()).item()  # noqa: E731
             out["rel_rms_vs_fp32"] = {"native": float(f"{rr(ours):.4g}"), "torch_library": float(f"{rr(lib):.4g}")}
             del ref, ours, lib
