@@ -171,6 +171,48 @@ __device__ __forceinline__ void sk_wait_flag(const unsigned *flag) {
     }
 }
 
+// Row-per-thread epilogues hold 64 contiguous bytes (32 bf16 columns) of their own row per
+// chunk; stored directly, one warp-wide 16-byte store touches 32 rows (32 half-filled
+// sectors).  A 4 x 4 transpose of the 16-byte pieces inside each lane quad (two shuffle
+// stages) makes lane 4g + j hold piece j of rows 4g .. 4g + 3, so each of the 4 stores
+// writes 8 rows x 64 contiguous bytes (full sectors, 4x fewer row segments per store).
+__device__ __forceinline__ uint4 shfl_xor_u4(uint4 v, int m) {
+    return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                      __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+// in: v[c] = piece c of this lane's row; out: v[i] = piece (lane & 3) of row (lane & ~3) + i
+__device__ __forceinline__ void quad_transpose(uint4 (&v)[4], int lane) {
+    const bool h2 = lane & 2, h1 = lane & 1;
+    uint4 a = shfl_xor_u4(h2 ? v[0] : v[2], 2), b = shfl_xor_u4(h2 ? v[1] : v[3], 2);
+    if (h2) {
+        v[0] = a;
+        v[1] = b;
+    } else {
+        v[2] = a;
+        v[3] = b;
+    }
+    a = shfl_xor_u4(h1 ? v[0] : v[1], 1);
+    b = shfl_xor_u4(h1 ? v[2] : v[3], 1);
+    if (h1) {
+        v[0] = a;
+        v[2] = b;
+    } else {
+        v[1] = a;
+        v[3] = b;
+    }
+}
+// all 32 lanes call this (shuffles); row_base = the warp's first row, col = first column
+// of the chunk; rows >= rows_end are not written
+__device__ __forceinline__ void store_rows_bf16x32(__nv_bfloat16 *out, int64_t ldo, int row_base, int rows_end,
+                                                   int col, int lane, uint4 (&v)[4]) {
+    quad_transpose(v, lane);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = row_base + (lane & ~3) + i;
+        if (row < rows_end) *(uint4 *)(out + (int64_t)row * ldo + col + (lane & 3) * 8) = v[i];
+    }
+}
+
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -467,11 +509,12 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                             aux4[v] = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
                         }
                     }
-                    if (epi.aux && live) {
-                        uint4 *dst = (uint4 *)(epi.aux + (int64_t)(m0 + lane) * epi.aux_ld + n0 + col);
+                    if (epi.aux) {   // warp-collective row stores (m0 = this warp's first row)
+                        uint4 pk[4];
 #pragma unroll
                         for (int v = 0; v < 4; ++v)
-                            dst[v] = make_uint4(aux4[2 * v].x, aux4[2 * v].y, aux4[2 * v + 1].x, aux4[2 * v + 1].y);
+                            pk[v] = make_uint4(aux4[2 * v].x, aux4[2 * v].y, aux4[2 * v + 1].x, aux4[2 * v + 1].y);
+                        store_rows_bf16x32(epi.aux, epi.aux_ld, m0, M, n0 + col, lane, pk);
                     }
                 }
                 if (p == NP - 1) tc_fence_before();
@@ -736,22 +779,22 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     continue;
                 }
                 if (sk_get) sk_add32(sk_slot, c0 / 32, lane, r);   // head + tail
-                if (!live) continue;
+                // bf16 row stores are warp-collective (quad transposes): dead rows ride along
+                if (!live && EPI != kStoreBF16 && EPI != kBF16Rope) continue;
                 const int n = n0 + c0;
                 if constexpr (EPI == kStoreBF16) {
-                    __nv_bfloat16 *o = (__nv_bfloat16 *)epi.out + (int64_t)m * epi.ldo + n;
+                    uint4 pk[4];
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
-                        uint4 pk;
-                        uint32_t *p = (uint32_t *)&pk;
+                        uint32_t *p = (uint32_t *)&pk[v];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[v * 8 + 2 * e]) * rs,
                                                                      __uint_as_float(r[v * 8 + 2 * e + 1]) * rs);
                             p[e] = *(uint32_t *)&h;
                         }
-                        *(uint4 *)(o + v * 8) = pk;
                     }
+                    store_rows_bf16x32((__nv_bfloat16 *)epi.out, epi.ldo, m0 + q * 32, M, n, lane, pk);
                 } else if constexpr (EPI == kBF16Rope) {
                     const int nl = epi.vt_period ? n % epi.vt_period : n;
                     if (epi.vt && nl >= epi.vt_col0) {
@@ -760,17 +803,18 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         const int64_t grp = epi.vt_period ? n / epi.vt_period : 0;
                         __nv_bfloat16 *dst = epi.vt + grp * epi.vt_layer_stride +
                                              ((b * epi.vt_heads + hv) * 128 + dim0) * epi.vt_ld + pos;
+                        if (live) {
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)   // lanes hold consecutive tokens: coalesced
-                            dst[(int64_t)e * epi.vt_ld] = __float2bfloat16(__uint_as_float(r[e]));
+                            for (int e = 0; e < 32; ++e)   // lanes hold consecutive tokens: coalesced
+                                dst[(int64_t)e * epi.vt_ld] = __float2bfloat16(__uint_as_float(r[e]));
+                        }
                         continue;
                     }
-                    __nv_bfloat16 *o = (__nv_bfloat16 *)epi.out + (int64_t)m * epi.ldo + n;
                     const bool rot = n < epi.rope_cols;
+                    uint4 pk4[4];
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
-                        uint4 pk;
-                        uint32_t *p = (uint32_t *)&pk;
+                        uint32_t *p = (uint32_t *)&pk4[v];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             float x0 = __uint_as_float(r[v * 8 + 2 * e]), x1 = __uint_as_float(r[v * 8 + 2 * e + 1]);
@@ -787,8 +831,8 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                             __nv_bfloat162 hh = __floats2bfloat162_rn(x0, x1);
                             p[e] = *(uint32_t *)&hh;
                         }
-                        *(uint4 *)(o + v * 8) = pk;
                     }
+                    store_rows_bf16x32((__nv_bfloat16 *)epi.out, epi.ldo, m0 + q * 32, M, n, lane, pk4);
                 } else if constexpr (EPI == kStoreF32 || EPI == kStoreF32Scale) {
                     float *o = (float *)epi.out + (int64_t)m * epi.ldo + n;
                     const float a = EPI == kStoreF32Scale ? epi.alpha : 1.0f;
