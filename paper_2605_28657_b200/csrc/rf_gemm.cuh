@@ -693,16 +693,17 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 uint32_t r[32];
                 tmem_ld32(tmem + lane_base + 384 + c * 32, r);
                 tmem_ld_wait();
-                if (live) {
-                    __nv_bfloat16 *dst = (__nv_bfloat16 *)epi.out + (int64_t)(m0 + row) * epi.ldo + n0 + c * 32;
+                uint4 pk[4];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v)
-                        *(uint4 *)(dst + v * 8) = make_uint4(
-                            pack_bf16(__uint_as_float(r[v * 8]) * inv_l, __uint_as_float(r[v * 8 + 1]) * inv_l),
-                            pack_bf16(__uint_as_float(r[v * 8 + 2]) * inv_l, __uint_as_float(r[v * 8 + 3]) * inv_l),
-                            pack_bf16(__uint_as_float(r[v * 8 + 4]) * inv_l, __uint_as_float(r[v * 8 + 5]) * inv_l),
-                            pack_bf16(__uint_as_float(r[v * 8 + 6]) * inv_l, __uint_as_float(r[v * 8 + 7]) * inv_l));
-                }
+                for (int v = 0; v < 4; ++v)
+                    pk[v] = make_uint4(
+                        pack_bf16(__uint_as_float(r[v * 8]) * inv_l, __uint_as_float(r[v * 8 + 1]) * inv_l),
+                        pack_bf16(__uint_as_float(r[v * 8 + 2]) * inv_l, __uint_as_float(r[v * 8 + 3]) * inv_l),
+                        pack_bf16(__uint_as_float(r[v * 8 + 4]) * inv_l, __uint_as_float(r[v * 8 + 5]) * inv_l),
+                        pack_bf16(__uint_as_float(r[v * 8 + 6]) * inv_l, __uint_as_float(r[v * 8 + 7]) * inv_l));
+                // the tile's live rows: its batch entry's rows (valid), clipped at M
+                store_rows_bf16x32((__nv_bfloat16 *)epi.out, epi.ldo, m0 + q * 32, m0 + min(valid, M - m0),
+                                   n0 + c * 32, lane, pk);
             }
             tc_fence_before();
             epi_sync();   // O read by every warp before the next tile's PV overwrites it
