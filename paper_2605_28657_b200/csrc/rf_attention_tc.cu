@@ -569,20 +569,19 @@ rf_attn_fa_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             uint32_t r[32];
             tmem_ld32(tO + c * 32, r);
             tmem_ld_wait();
-            if (qrow < Nq) {
-                __nv_bfloat16 *dst = out + ((int64_t)b * Nq + qrow) * ldo + h * 128 + c * 32;
+            uint4 pk[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t w[4];
+            for (int q = 0; q < 4; ++q) {
+                uint32_t *w = (uint32_t *)&pk[q];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]) * inv_l,
-                                                                  __uint_as_float(r[q * 8 + 2 * e + 1]) * inv_l);
-                        w[e] = *(uint32_t *)&hh;
-                    }
-                    *(uint4 *)(dst + q * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]) * inv_l,
+                                                              __uint_as_float(r[q * 8 + 2 * e + 1]) * inv_l);
+                    w[e] = *(uint32_t *)&hh;
                 }
             }
+            // warp-collective: 8 query rows x 64 contiguous bytes per store (rows >= Nq skipped)
+            store_rows_bf16x32(out + (int64_t)b * Nq * ldo, ldo, qrow - lane, Nq, h * 128 + c * 32, lane, pk);
         }
     }
     tc_fence_before();
@@ -842,20 +841,19 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             uint32_t r[32];
             tmem_ld32(tO + c * 32, r);
             tmem_ld_wait();
-            if (qrow < Nq) {
-                __nv_bfloat16 *dst = out + ((int64_t)b * Nq + qrow) * ldo + h * 128 + c * 32;
+            uint4 pk[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t w[4];
+            for (int q = 0; q < 4; ++q) {
+                uint32_t *w = (uint32_t *)&pk[q];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]) * inv_l,
-                                                                  __uint_as_float(r[q * 8 + 2 * e + 1]) * inv_l);
-                        w[e] = *(uint32_t *)&hh;
-                    }
-                    *(uint4 *)(dst + q * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]) * inv_l,
+                                                              __uint_as_float(r[q * 8 + 2 * e + 1]) * inv_l);
+                    w[e] = *(uint32_t *)&hh;
                 }
             }
+            // warp-collective: 8 query rows x 64 contiguous bytes per store (rows >= Nq skipped)
+            store_rows_bf16x32(out + (int64_t)b * Nq * ldo, ldo, qrow - lane, Nq, h * 128 + c * 32, lane, pk);
         }
     }
     tc_fence_before();

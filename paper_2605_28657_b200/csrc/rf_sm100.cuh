@@ -251,4 +251,47 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
         : "memory");
 }
 
+// ------------------------------------------------------- coalesced row stores ----
+// Row-per-thread epilogues hold 64 contiguous bytes (32 bf16 columns) of their own row per
+// chunk; stored directly, one warp-wide 16-byte store touches 32 rows (32 half-filled
+// sectors).  A 4 x 4 transpose of the 16-byte pieces inside each lane quad (two shuffle
+// stages) makes lane 4g + j hold piece j of rows 4g .. 4g + 3, so each of the 4 stores
+// writes 8 rows x 64 contiguous bytes (full sectors, 4x fewer row segments per store).
+__device__ __forceinline__ uint4 shfl_xor_u4(uint4 v, int m) {
+    return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                      __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+// in: v[c] = piece c of this lane's row; out: v[i] = piece (lane & 3) of row (lane & ~3) + i
+__device__ __forceinline__ void quad_transpose(uint4 (&v)[4], int lane) {
+    const bool h2 = lane & 2, h1 = lane & 1;
+    uint4 a = shfl_xor_u4(h2 ? v[0] : v[2], 2), b = shfl_xor_u4(h2 ? v[1] : v[3], 2);
+    if (h2) {
+        v[0] = a;
+        v[1] = b;
+    } else {
+        v[2] = a;
+        v[3] = b;
+    }
+    a = shfl_xor_u4(h1 ? v[0] : v[1], 1);
+    b = shfl_xor_u4(h1 ? v[2] : v[3], 1);
+    if (h1) {
+        v[0] = a;
+        v[2] = b;
+    } else {
+        v[1] = a;
+        v[3] = b;
+    }
+}
+// all 32 lanes call this (shuffles); row_base = the warp's first row, col = first column
+// of the chunk; rows >= rows_end are not written
+__device__ __forceinline__ void store_rows_bf16x32(__nv_bfloat16 *out, int64_t ldo, int row_base, int rows_end,
+                                                   int col, int lane, uint4 (&v)[4]) {
+    quad_transpose(v, lane);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = row_base + (lane & ~3) + i;
+        if (row < rows_end) *(uint4 *)(out + (int64_t)row * ldo + col + (lane & 3) * 8) = v[i];
+    }
+}
+
 }  // namespace rf::sm100
