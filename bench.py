@@ -155,9 +155,14 @@ def solve_bytes_per_row(toy: bool):
     return T * D * ((7 * 8) if toy else (4 * 8 + 4))
 
 
-def timed_ticks(pipe, steps, flush, stream):
+def timed_ticks(pipe, steps, flush, stream, phases=False):
+    """Device time of `steps` ticks (CUDA events on the pipeline stream around each tick, L2
+    flushed before each, outside the events).  phases=True also records the pipeline's
+    per-phase events in the same ticks (returned as mean ms per phase), so the roofline's
+    model time and `value` come from the same ticks."""
     import torch
 
+    ph = pipe.enable_phase_timing(True) if phases else None
     pairs, completions, launches = [], 0, 0
     for _ in range(steps):
         with torch.cuda.stream(stream):
@@ -170,20 +175,11 @@ def timed_ticks(pipe, steps, flush, stream):
         completions += len(recs)
         launches += pipe.launches_last_tick
     torch.cuda.synchronize()
-    return sum(a.elapsed_time(b) for a, b in pairs), completions, launches
-
-
-def phase_times(pipe, steps, flush, stream):
-    import torch
-
-    phases = pipe.enable_phase_timing(True)
-    for _ in range(steps):
-        with torch.cuda.stream(stream):
-            flush.fill_(1)
-        pipe.tick()
-    torch.cuda.synchronize()
-    pipe.enable_phase_timing(False)
-    return {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in phases.items()}
+    total = sum(a.elapsed_time(b) for a, b in pairs)
+    if phases:
+        pipe.enable_phase_timing(False)
+        return total, completions, launches, {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in ph.items()}
+    return total, completions, launches
 
 
 def decode_240s(codec, world, rank, flush, hbm_peak, iters=10):
@@ -262,9 +258,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
-        dev_ms, completions, launches = timed_ticks(pipe, args.steps, flush, st)
+        dev_ms, completions, launches, phase_ms = timed_ticks(pipe, args.steps, flush, st, phases=True)
     clocks = clk.summary()
-    phase_ms = phase_times(pipe, max(4, args.steps // 4), flush, st)
     dit_flops = dcfg.flops_per_forward(DEPTH, T)
     dit_tflops = dit_flops / (phase_ms["model"] * 1e-3) / 1e12
 
@@ -334,7 +329,9 @@ def run_ours(args):
             tp.tick()
         torch.cuda.synchronize()
         t_ms, t_done, t_launch = timed_ticks(tp, 64, flush, tp.stream)
-        t_phase = phase_times(tp, 16, flush, tp.stream)
+        # phases from separate ticks: at ~0.13 ms per tick the phase events would be a
+        # visible part of the timed region
+        t_phase = timed_ticks(tp, 16, flush, tp.stream, phases=True)[3]
         sb = DEPTH * solve_bytes_per_row(True)
         toy = {"value": round(t_done / (t_ms * 1e-3), 2), "unit": UNIT, "ms_per_step": round(t_ms / 64, 5),
                "phase_ms": {k: round(v, 5) for k, v in t_phase.items()},
