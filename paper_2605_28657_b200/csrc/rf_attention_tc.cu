@@ -873,6 +873,8 @@ int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const voi
     if (!rc)
         rc = make_tmap_bf16_2d(&p->tvt, vt, (uint64_t)Nk_pad, (uint64_t)B * Hkv * 128, (uint64_t)Nk_pad * 2, 64, 128);
     if (!rc) rc = make_tmap_bf16_2d(&p->tk64, k, (uint64_t)k_cols, (uint64_t)B * Nk, (uint64_t)ldk * 2, 64, 64);
+    if (!rc)
+        rc = make_tmap_bf16_2d(&p->tvt64, vt, (uint64_t)Nk_pad, (uint64_t)B * Hkv * 128, (uint64_t)Nk_pad * 2, 64, 64);
     p->B = B;
     p->Nq = Nq;
     p->Nk = Nk;

@@ -321,6 +321,9 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     // where 256-wide tiles leave the second wave mostly idle; single-CTA 128 x 128 tiles
     // when M is small (the cross-attention K/V of 128 tokens per row).
     auto bn_for = [](int64_t n) { return (n >= 4096 && n % 256 == 0) ? 256 : 128; };
+    // cross-Q projection + cross-attention epilogue on CTA pairs (256-row tiles, cta_group::2
+    // attention MMAs); RF_DIT_XATT_PAIR=0 keeps single-CTA 128-row tiles (A/B timing)
+    const int xattn_cg = (getenv("RF_DIT_XATT_PAIR") && atoi(getenv("RF_DIT_XATT_PAIR")) == 0) ? 1 : 2;
     int rc = 0;
     auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
         if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N), M >= 1024 ? 2 : 1);
@@ -346,7 +349,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
         plan(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_qc[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D);
-        if (!rc) rc = gemm_plan(&d->p_qcx[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D, D, D, 128, 1);
+        if (!rc) rc = gemm_plan(&d->p_qcx[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D, D, D, 128, xattn_cg);
         plan(&d->p_oc[l], d->att, woc + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_gu[l], d->a, wgu + l * 2 * (int64_t)c.mlp_hidden * D, BN, 2 * (int64_t)c.mlp_hidden, D);
         plan(&d->p_down[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, BN, D, c.mlp_hidden);
@@ -505,7 +508,7 @@ static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) 
         if (!(skip & 1) && !d.fuse_norm2) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
         const bool xattn = d.fuse_xattn && d.tc_attention;
         if (xattn && !(skip & 32)) {   // query projection + cross-attention in one kernel
-            const XAttn xa{&d.a_cross[l].tk, &d.a_cross[l].tvt, (int)N, (int)B, (int)Nc,
+            const XAttn xa{&d.a_cross[l].tk, &d.a_cross[l].tvt, &d.a_cross[l].tk64, &d.a_cross[l].tvt64, (int)N, (int)B, (int)Nc,
                            c.n_heads / c.n_kv_heads, c.n_kv_heads};
             RF_TRY(gemm_run(d.p_qcx[l], 6 /* cross-attention epilogue */, d.att, d.q_dim, nullptr, 0, 1, 1.f, st,
                             nullptr, 0, M, nullptr, d.fuse_norm2 ? &nf_in : nullptr, &xa));

@@ -213,20 +213,21 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
         e.rs_eps = nf->rs_eps;
     }
     if (epi == gemm::kCrossAttn) {
-        if (!xa || p.bn != 128 || p.cg != 1 || xa->n_keys > 128 || xa->n_keys < 1 || xa->rows_per_batch < 1 ||
-            p.N % 128) {
-            set_error("gemm: cross-attention epilogue needs 128-wide single-CTA tiles and <= 128 keys");
+        if (!xa || p.bn != 128 || xa->n_keys > 128 || xa->n_keys < 1 || xa->rows_per_batch < 1 || p.N % 128 ||
+            (p.cg == 2 && (!xa->tk64 || !xa->tvt64))) {
+            set_error("gemm: cross-attention epilogue needs 128-wide tiles and <= 128 keys");
             return RF_EINVAL;
         }
-        p.tk = *xa->tk;
-        p.tvt = *xa->tvt;
+        p.tk = p.cg == 2 ? *xa->tk64 : *xa->tk;
+        p.tvt = p.cg == 2 ? *xa->tvt64 : *xa->tvt;
         e.x_rpb = xa->rows_per_batch;
-        e.x_mtpb = (xa->rows_per_batch + gemm::BM - 1) / gemm::BM;
+        e.x_mtpb = (xa->rows_per_batch + gemm::BM * p.cg - 1) / (gemm::BM * p.cg);
         e.x_batches = xa->batches;
         e.x_nk = xa->n_keys;
         e.x_group = xa->group;
         e.x_hkv = xa->kv_heads;
         e.x_scale = 1.4426950408889634f / sqrtf(128.f);
+        if (p.cg == 2) return launch<128, gemm::kCrossAttn, 2>(p, e, st);
         return launch<128, gemm::kCrossAttn, 1>(p, e, st);
     }
     if (p.sk) {

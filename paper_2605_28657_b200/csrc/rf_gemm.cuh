@@ -124,7 +124,7 @@ struct Cfg {
     static constexpr int C_COLS = CC;                                           // staged per pass
     static constexpr uint32_t C_WARP_BYTES = TMA_C ? 32u * C_COLS * 4u : (TMA_O ? 32u * 128u * 2u : 0u);
     static constexpr uint32_t GATE_WARP_BYTES = TMA_C ? 2u * BN * 4u : 0u;   // the two gate rows a warp can touch
-    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + 4 * GATE_WARP_BYTES + (XATT ? 3u * 32768u : 0u);
+    static constexpr uint32_t C_BYTES = 4 * C_WARP_BYTES + 4 * GATE_WARP_BYTES + (XATT ? (CG == 1 ? 3u * 32768u : 65536u) : 0u);
     // as many operand stages as fit next to the epilogue staging (227 KB opt-in limit)
     static constexpr uint32_t BUDGET = 232448u - 1024u - 512u - C_BYTES;
     static constexpr int STAGES = (int)(BUDGET / STAGE_BYTES) > 10 ? 10 : (int)(BUDGET / STAGE_BYTES);
@@ -196,9 +196,9 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *cfull = tempty + 2;            // [4] one per epilogue warp (TMA_C)
-    uint64_t *xbar = cfull + 4;              // [3] kCrossAttn: K/V loaded, S done, O done
-    uint32_t *tmem_slot = (uint32_t *)(xbar + 3);
-    static_assert(!C::XATT || (CG == 1 && BN == 128), "cross-attention epilogue: single-CTA 128-wide tiles");
+    uint64_t *xbar = cfull + 4;              // [5] kCrossAttn: K/V loaded, S done, O done, Q ready, P ready
+    uint32_t *tmem_slot = (uint32_t *)(xbar + 5);
+    static_assert(!C::XATT || BN == 128, "cross-attention epilogue: 128-wide tiles (one query head)");
     constexpr uint32_t TMEM_COLS = C::XATT ? 512 : 2 * BN;   // + S and O of the epilogue attention
 
     RF_GTRACE(15);
@@ -218,6 +218,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         }
         for (int i = 0; i < 4; ++i) mbar_init(&cfull[i], 1);
         for (int i = 0; i < 3; ++i) mbar_init(&xbar[i], 1);
+        for (int i = 3; i < 5; ++i) mbar_init(&xbar[i], CG);   // one arrival per CTA of the pair
         if constexpr (C::XATT) {
             tma_prefetch(&tma_k);
             tma_prefetch(&tma_vt);
@@ -255,7 +256,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     // first row of tile t (kCrossAttn: tiles never straddle two batch entries)
     auto row0 = [&](int t) {
         const int mt = t % num_m;
-        if constexpr (C::XATT) return (mt / epi.x_mtpb) * epi.x_rpb + (mt % epi.x_mtpb) * BM;
+        if constexpr (C::XATT) return (mt / epi.x_mtpb) * epi.x_rpb + (mt % epi.x_mtpb) * TM + (int)rank * BM;
         return mt * TM + (int)rank * BM;
     };
     const int num_tiles = num_m * num_n;
@@ -515,27 +516,48 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         }
         if (lane == 0) bulk_wait0();
     } else if constexpr (C::XATT) {
-        // Cross-attention in the epilogue of the query projection.  Per tile (128 rows of one
+        // Cross-attention in the epilogue of the query projection.  Per tile (TM rows of one
         // batch entry x one query head): Q (accumulator, fused-norm scaled) -> bf16 SW128 tile
-        // in smem; S = Q K^T (128 x 128, issued by one epilogue thread into TMEM columns
-        // 256..383 while the MMA warp already runs the next tile's main loop); row softmax
-        // (one row per thread, a single key tile: no rescaling); P (bf16) over S in TMEM;
-        // O = P V (TS MMA into columns 384..511); O / l -> bf16 att.  K and V^T of the next
-        // tile are prefetched by TMA as soon as this tile's MMAs have read them.
+        // in smem; S = Q K^T (issued by one epilogue thread into TMEM columns 256..383 while
+        // the MMA warp already runs the next tile's main loop); row softmax (one row per
+        // thread, a single key tile: no rescaling); P (bf16) over S in TMEM; O = P V (TS MMA
+        // into columns 384..511); O / l -> bf16 att.  K and V^T of the next tile are
+        // prefetched by TMA as soon as this tile's MMAs have read them.
+        // CG = 2 (CTA pairs, 256-row tiles): the attention MMAs are cta_group::2 as well, M =
+        // 256 over both CTAs' Q / P rows; each CTA stages half of K (64 keys) and half of V^T
+        // (64 dims), the leader CTA's thread issues S and PV once both CTAs' Q (P) are ready
+        // (xq / xp count one arrival per CTA), and the commits multicast to both CTAs.
         const int q = warp & 3;
-        const int row = q * 32 + lane;                       // row within the tile
+        const int row = q * 32 + lane;                       // row within this CTA's 128
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        uint8_t *sQ = sC, *sK = sC + 32768, *sV = sC + 65536;
-        uint64_t *xk = xbar, *xs = xbar + 1, *xo = xbar + 2;
-        const bool leader = q == 0 && lane == 0;
-        constexpr uint32_t idS = idesc_bf16(128, 128);
+        constexpr uint32_t KV_HALF = CG == 1 ? 16384u : 8192u;   // one 64-dim (64-key) SW128 half
+        uint8_t *sQ = sC, *sK = sC + 32768, *sV = sC + 32768 + 2 * KV_HALF;
+        uint64_t *xk = xbar, *xs = xbar + 1, *xo = xbar + 2, *xq = xbar + 3, *xp = xbar + 4;
+        const bool leader = q == 0 && lane == 0;                 // per CTA
+        const bool issuer = leader && rank == 0;                 // issues the attention MMAs
+        constexpr uint32_t idS = idesc_bf16(TM, 128);
         auto load_kv = [&](int t) {
             const int mt = t % num_m, b = mt / epi.x_mtpb, hk = (t / num_m) / epi.x_group;
-            mbar_expect_tx(xk, 65536);
-            tma_load_2d(sK, &tma_k, xk, hk * 128, b * epi.x_nk);
-            tma_load_2d(sK + 16384, &tma_k, xk, hk * 128 + 64, b * epi.x_nk);
-            tma_load_2d(sV, &tma_vt, xk, 0, (b * epi.x_hkv + hk) * 128);
-            tma_load_2d(sV + 16384, &tma_vt, xk, 64, (b * epi.x_hkv + hk) * 128);
+            if constexpr (CG == 1) {
+                mbar_expect_tx(xk, 65536);
+                tma_load_2d(sK, &tma_k, xk, hk * 128, b * epi.x_nk);
+                tma_load_2d(sK + 16384, &tma_k, xk, hk * 128 + 64, b * epi.x_nk);
+                tma_load_2d(sV, &tma_vt, xk, 0, (b * epi.x_hkv + hk) * 128);
+                tma_load_2d(sV + 16384, &tma_vt, xk, 64, (b * epi.x_hkv + hk) * 128);
+            } else {   // this CTA's 64 keys of K and 64 dims of V^T (maps with 64 x 64 boxes)
+                if (rank == 0) mbar_expect_tx(xk, 2 * 4 * KV_HALF);
+                const uint32_t fb = mapa_shared(xk, 0);
+                tma_load_2d_pair(sK, &tma_k, fb, hk * 128, b * epi.x_nk + (int)rank * 64);
+                tma_load_2d_pair(sK + KV_HALF, &tma_k, fb, hk * 128 + 64, b * epi.x_nk + (int)rank * 64);
+                tma_load_2d_pair(sV, &tma_vt, fb, 0, (b * epi.x_hkv + hk) * 128 + (int)rank * 64);
+                tma_load_2d_pair(sV + KV_HALF, &tma_vt, fb, 64, (b * epi.x_hkv + hk) * 128 + (int)rank * 64);
+            }
+        };
+        auto arrive_leader = [&](uint64_t *bar) {   // one arrival per CTA on the leader's barrier
+            if constexpr (CG == 2)
+                mbar_arrive_cluster(mapa_shared(bar, 0));
+            else
+                mbar_arrive(bar);
         };
         auto epi_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
         int acc = 0, it = 0;
@@ -543,7 +565,8 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         if (leader && unit < num_tiles) load_kv(unit);
         for (int t = unit; t < num_tiles; t += units, ++it) {
             const int m0 = row0(t), n0 = (t / num_m) * BN;
-            const int valid = min(BM, epi.x_rpb - ((t % num_m) % epi.x_mtpb) * BM);
+            // this CTA's rows of the tile that belong to its batch entry
+            const int valid = max(0, min(BM, epi.x_rpb - (((t % num_m) % epi.x_mtpb) * TM + (int)rank * BM)));
             const bool live = row < valid && m0 + row < M;
             float rs = 1.0f;   // the fused RMSNorm of the query projection's input rows
             if (epi.rs_part && live) {
@@ -575,22 +598,30 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             tc_fence_before();
             fence_proxy_async_smem();   // Q (generic proxy) -> visible to the tensor core
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);   // the accumulator is free for tile i + 2
+            if (lane == 0) arrive_leader(&tempty[acc]);   // the accumulator is free for tile i + 2
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
             epi_sync();
-            if (leader) {
+            if (leader) arrive_leader(xq);
+            if (issuer) {
+                mbar_wait(xq, xph);
                 mbar_wait(xk, xph);
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
                     const uint64_t ad = sdesc_sw128(sQ + (ks >> 2) * 16384) + (uint64_t)((ks & 3) * 2);
-                    const uint64_t bd = sdesc_sw128(sK + (ks >> 2) * 16384) + (uint64_t)((ks & 3) * 2);
-                    umma_bf16(tmem + 256, ad, bd, idS, ks > 0);
+                    const uint64_t bd = sdesc_sw128(sK + (ks >> 2) * KV_HALF) + (uint64_t)((ks & 3) * 2);
+                    if constexpr (CG == 2)
+                        umma_bf16_pair(tmem + 256, ad, bd, idS, ks > 0);
+                    else
+                        umma_bf16(tmem + 256, ad, bd, idS, ks > 0);
                 }
-                umma_commit(xs);
+                if constexpr (CG == 2)
+                    umma_commit_pair(xs);
+                else
+                    umma_commit(xs);
             }
             mbar_wait(xs, xph);
             tc_fence_after();
@@ -631,14 +662,22 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             tmem_st_wait();
             tc_fence_before();
             epi_sync();
-            if (leader) {
+            if (leader) arrive_leader(xp);
+            if (issuer) {
+                mbar_wait(xp, xph);
                 tc_fence_after();
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
-                    const uint64_t bd = sdesc_sw128(sV + (ks >> 2) * 16384) + (uint64_t)((ks & 3) * 2);
-                    umma_bf16_ts(tmem + 384, tmem + 256 + ks * 8, bd, idS, ks > 0);
+                    const uint64_t bd = sdesc_sw128(sV + (ks >> 2) * KV_HALF) + (uint64_t)((ks & 3) * 2);
+                    if constexpr (CG == 2)
+                        umma_bf16_ts_pair(tmem + 384, tmem + 256 + ks * 8, bd, idS, ks > 0);
+                    else
+                        umma_bf16_ts(tmem + 384, tmem + 256 + ks * 8, bd, idS, ks > 0);
                 }
-                umma_commit(xo);
+                if constexpr (CG == 2)
+                    umma_commit_pair(xo);
+                else
+                    umma_commit(xo);
             }
             mbar_wait(xo, xph);
             tc_fence_after();

@@ -55,6 +55,7 @@ struct NormFuse {
 // query rows per batch entry, n_keys keys per entry, K / V^T through the attention maps.
 struct XAttn {
     const CUtensorMap *tk, *tvt;
+    const CUtensorMap *tk64, *tvt64;   // 64 x 64 boxes: one CTA's half of K / V^T on a CTA pair
     int rows_per_batch, batches, n_keys, group, kv_heads;
 };
 
@@ -66,6 +67,7 @@ int gemm_run(const GemmPlan &p, int epi, void *out, int64_t ldo, const float *ga
 // tcgen05 attention (rf_attention_tc.cu): tensor maps over Q, K and V^T built once.
 struct AttnPlan {
     CUtensorMap tq, tk, tvt, tk64;   // tk64: 64-key boxes (rf_attn_fa64_kernel)
+    CUtensorMap tvt64;               // 64-key x 64-dim boxes (pair cross-attention epilogue)
     int B, Nq, Nk, Nk_pad, H, Hkv;
 };
 int attn_plan(AttnPlan *p, const void *q, int64_t ldq_elems, int64_t q_cols, const void *k, int64_t ldk_elems,
