@@ -160,6 +160,32 @@ def test_full_size_dit_vs_fp32_oracle(dit_mod):
     assert rel_rms(out, ref) < 3e-2   # 24 layers of bf16 operands
 
 
+@pytest.mark.parametrize("var,exact", [("RF_DIT_XATT_PAIR", True), ("RF_DIT_L2_PERSIST", True),
+                                       ("RF_DIT_FUSE_XATTN", False)])
+def test_full_size_dit_kernel_variants(dit_mod, var, exact):
+    """The same forward with a kernel-level variant switched off (env read at rf_dit_create).
+    Cross-Q + cross-attention on single CTAs instead of CTA pairs, and no L2 residency
+    window: every output element is the same sequence of fp32 operations, so the velocities
+    are bit-identical.  Cross-attention as its own kernel (its softmax is organised
+    differently): equal within bf16 rounding, rel-RMS < 1e-2."""
+    import os
+
+    base = dit_mod.DiT(dit_mod.DiTConfig(), frames=1500, max_rows=4)
+    os.environ[var] = "0"
+    try:
+        alt = dit_mod.DiT(dit_mod.DiTConfig(), frames=1500, max_rows=4, weights=base.weights)
+    finally:
+        del os.environ[var]
+    xs, ts, conds = _inputs(base, 4, 1500, 64, seed=5)
+    a = base.forward(xs, ts, conds).clone()
+    b = alt.forward(xs, ts, conds).clone()
+    assert torch.isfinite(a).all()
+    if exact:
+        assert torch.equal(a, b)
+    else:
+        assert rel_rms(b, a) < 1e-2
+
+
 def test_full_size_dit_is_deterministic(dit_mod):
     """Repeated full-size forwards (replays of the captured graph, back to back) are
     bit-identical and finite -- a data race between warp-specialised roles (TMA, MMA,
