@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-toy", action="store_true")
     ap.add_argument("--no-library-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     return ap.parse_args()
 
 
@@ -228,6 +229,78 @@ def decode_240s(codec, world, rank, flush, hbm_peak, iters=10):
             "flops": frames * 344064, "sharded_equals_full_decode": exact}
 
 
+def config_legs(rf, dit_mod, model, rank, flush, ticks=60):
+    """Configs 3 and 4 on the same DiT weights, device time per tick as for
+    `value` (events on the pipeline stream, L2 flushed between ticks outside the events).
+    config 3: ring depth 8, S=8, one set_denoise per tick from the reference's 60-value
+      slider sweep (bench.py:354-357: 1.0 -> 0.5 -> 1.0), so in-flight slots carry
+      different baked schedules; 8 DiT rows per tick, one completion per tick.
+    config 4: depth 4, request sde_denoise_curve = linspace(0, 1, T) with a source (per-frame
+      source blending), and every tick a shared-curve write
+      clip(linspace(0, 1, T) * (0.5 + 0.5 sin(2 pi k / 16)), 0, 1) visible from that tick."""
+    import numpy as np
+    import torch
+
+    sweep = [1.0 - 0.5 * i / 30 for i in range(31)] + [0.5 + 0.5 * j / 29 for j in range(1, 30)]
+    out = {}
+    m8 = dit_mod.DiT(dit_mod.DiTConfig(), frames=T, max_rows=8, weights=model.weights)
+    p3 = rf.StreamPipeline(rf.PipelineConfig(depth=8, steps=STEPS, frames=T, channels=D, seed=rank),
+                           request=make_request(rf, rank), velocity_model=dit_mod.DiTVelocity(m8))
+    for k in range(4 * STEPS):
+        p3.set_denoise(sweep[k % len(sweep)])
+        p3.tick()
+    torch.cuda.synchronize()
+    ev, done, sched = [], 0, set()
+    for k in range(ticks):
+        p3.set_denoise(sweep[k % len(sweep)])
+        with torch.cuda.stream(p3.stream):
+            flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(p3.stream)
+        done += len(p3.tick())
+        b.record(p3.stream)
+        ev.append((a, b))
+        sched.update(s.schedule.schedule_id for s in p3._slots if s is not None)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    out["config3"] = {"workload": "depth 8, S=8, 60-s latent, DiT, one set_denoise per tick over the reference's "
+                                  "60-value slider sweep (per-slot heterogeneous schedules)",
+                      "value": round(done / (ms * 1e-3), 3), "unit": UNIT, "ms_per_step": round(ms / ticks, 4),
+                      "ticks": ticks, "completions": done, "distinct_schedules_in_flight": len(sched)}
+    del p3, m8
+    torch.cuda.empty_cache()
+
+    lin = np.linspace(0.0, 1.0, T)
+    req = make_request(rf, rank)
+    req4 = rf.GenerationRequest(conditions=req.conditions, curves=rf.CurveSet(sde_denoise_curve=lin))
+    p4 = rf.StreamPipeline(rf.PipelineConfig(depth=DEPTH, steps=STEPS, frames=T, channels=D, seed=rank),
+                           request=req4, velocity_model=dit_mod.DiTVelocity(model))
+    shared = lambda k: np.clip(lin * (0.5 + 0.5 * np.sin(2 * np.pi * k / 16)), 0.0, 1.0)  # noqa: E731
+    for k in range(4 * STEPS):
+        p4.set_shared_curve("sde_denoise_curve", shared(k))
+        p4.tick()
+    torch.cuda.synchronize()
+    ev, done = [], 0
+    for k in range(ticks):
+        p4.set_shared_curve("sde_denoise_curve", shared(k))   # host -> device, visible from this tick
+        with torch.cuda.stream(p4.stream):
+            flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(p4.stream)
+        done += len(p4.tick())
+        b.record(p4.stream)
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    out["config4"] = {"workload": "depth 4, S=8, 60-s latent, DiT, request sde_denoise_curve = linspace(0,1,T) "
+                                  "with source (per-frame blend), a shared-curve write every tick",
+                      "value": round(done / (ms * 1e-3), 3), "unit": UNIT, "ms_per_step": round(ms / ticks, 4),
+                      "ticks": ticks, "completions": done}
+    del p4
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -291,6 +364,7 @@ def run_ours(args):
     pipe.set_shared_curve("sde_denoise_curve", 1.0)
 
     # ---- windowed decode (3-s window + overlap 15) of the last completion ----
+    configs = None if args.no_configs else config_legs(rf, dit_mod, model, rank, flush)
     lat = pipe._last_emitted
     with torch.cuda.stream(st):
         for _ in range(3):
@@ -393,6 +467,8 @@ def run_ours(args):
         line["toy_path"] = toy
     if library is not None:
         line["library_baseline"] = library
+    if configs is not None:
+        line["other_configs"] = configs
     if not args.no_cpu_baseline:
         # the same workload (config 2 with the DiT) on the box's host cores, bounded sample
         line["cpu_baseline"] = cpu_dit_baseline(args.cpu_seconds, os.cpu_count() or 1)
