@@ -21,12 +21,18 @@ class NoDeviceError(RuntimeError):
     pass
 
 
+_checked = False
+
+
 def device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise NoDeviceError(
-            "paper_2605_28657_b200 computes only on a CUDA device (sm_100a); none is available"
-        )
-    _native.load()
+    global _checked
+    if not _checked:   # availability and the library are checked once per process
+        if not torch.cuda.is_available():
+            raise NoDeviceError(
+                "paper_2605_28657_b200 computes only on a CUDA device (sm_100a); none is available"
+            )
+        _native.load()
+        _checked = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
@@ -53,10 +59,11 @@ def to_host(x) -> np.ndarray:
     return np.asarray(x)
 
 
-def workspace(nbytes: int, tag: str = "default", dev=None) -> torch.Tensor:
-    """A cached uint8 device buffer of at least ``nbytes`` for the current stream's work."""
+def workspace(nbytes: int, tag: str = "default", dev=None, stream: int = None) -> torch.Tensor:
+    """A cached uint8 device buffer of at least ``nbytes`` for the work of one stream (the
+    current stream unless a stream handle is given)."""
     dev = dev or device()
-    key = (dev.index, tag, torch.cuda.current_stream(dev).cuda_stream)
+    key = (dev.index, tag, torch.cuda.current_stream(dev).cuda_stream if stream is None else stream)
     with _ws_lock:
         buf = _workspaces.get(key)
         if buf is None or buf.numel() < nbytes:

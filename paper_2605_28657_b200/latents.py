@@ -169,10 +169,12 @@ def _numel(shape) -> int:
     return n
 
 
-def fill_normals(draws, status: torch.Tensor = None) -> None:
-    """Batched bit-exact normal fill. ``draws`` = [(key, out_tensor_f64), ...] on one device."""
+def fill_normals(draws, status: torch.Tensor = None, stream: int = None) -> None:
+    """Batched bit-exact normal fill. ``draws`` = [(key, out_tensor_f64), ...] on one device;
+    ``stream``: the CUDA stream handle to run on (default: the current stream)."""
     if not draws:
         return
+    st = _device.current_stream_handle() if stream is None else stream
     lib = _native.load()
     arr = (_native.RfDraw * len(draws))()
     for i, (key, out) in enumerate(draws):
@@ -182,12 +184,12 @@ def fill_normals(draws, status: torch.Tensor = None) -> None:
         arr[i].out = out.data_ptr()
     nbytes = lib.rf_normal_workspace_bytes(arr, len(draws))
     dev = draws[0][1].device
-    ws = _device.workspace(nbytes, "noise", dev)
+    ws = _device.workspace(nbytes, "noise", dev, st)
     own_status = status is None
     if own_status:
         status = torch.zeros(1, dtype=torch.int32, device=dev)
-    _native.check(lib.rf_normal_fill(arr, len(draws), ws.data_ptr(), ws.numel(), status.data_ptr(),
-                                     _device.current_stream_handle()), "rf_normal_fill")
+    _native.check(lib.rf_normal_fill(arr, len(draws), ws.data_ptr(), ws.numel(), status.data_ptr(), st),
+                  "rf_normal_fill")
     if own_status:
         flags = int(status.item())
         if flags & _native.RF_STATUS_NOISE_SHORT:

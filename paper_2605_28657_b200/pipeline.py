@@ -545,7 +545,7 @@ class StreamPipeline:
                 rows.append(row)
         if draws:
             ev = self._phase_begin("noise")
-            fill_normals(draws, self._status)
+            fill_normals(draws, self._status, self._stream.cuda_stream)
             self._phase_end("noise", ev)
             self.launches_last_tick += 2
         lib = _native.load()
@@ -677,7 +677,7 @@ class StreamPipeline:
                 admits[j].source = None
                 admits[j].denoise = 1.0
         ev = self._phase_begin("admit")
-        fill_normals(draws, self._status)
+        fill_normals(draws, self._status, self._stream.cuda_stream)
         lib = _native.load()
         _native.check(lib.rf_admit_init(admits, len(slots), slots[0].x.numel(), self._stream.cuda_stream),
                       "rf_admit_init")
