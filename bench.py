@@ -520,8 +520,9 @@ def cpu_baseline(seconds, processes=1):
 
 def cpu_dit_baseline(seconds, threads, max_ticks=None):
     """Config 2 on the host CPU: the reference's tick (oracle/ringflow_np.py, float64 numpy)
-    with the DiT in its model slot (oracle/dit_fp32.py: the same network, fp32 torch on all
-    `threads` host threads; one forward per ring row per tick).  The ring is filled with the
+    with the DiT in its model slot (oracle/dit_fp32.py: the same network with bf16 GEMM and
+    attention operands -- the precision of the GPU arm and the CPU's fastest path (AMX) --
+    torch on all `threads` host threads; one forward per ring row per tick).  The ring is filled with the
     toy model first (cheap), then steady-state DiT ticks are timed: at least one, then until
     `seconds` or `max_ticks`.  completions/s = row-steps / S / wall (every completion is S
     row-steps; at depth 4 one completes every other tick)."""
@@ -539,7 +540,7 @@ def cpu_dit_baseline(seconds, threads, max_ticks=None):
     pipe = O.Pipeline(depth=DEPTH, steps=STEPS, frames=T, channels=D, seed=0, request=req)
     for _ in range(4 * STEPS):
         pipe.tick()
-    pipe.model = CpuDiTVelocity(DiTConfig(), T)
+    pipe.model = CpuDiTVelocity(DiTConfig(), T, bf16=True)   # the fastest CPU path (bf16 AMX GEMMs)
     pipe.tick()   # untimed: first-touch of the fp32 weights
     row_steps, ticks = 0, 0
     t0 = time.perf_counter()
@@ -551,7 +552,8 @@ def cpu_dit_baseline(seconds, threads, max_ticks=None):
     return {"value": round(row_steps / STEPS / wall, 5), "unit": UNIT, "cores": threads, "kind": "port",
             "ticks": ticks,
             "sample": f"config 2 on the host CPU: oracle/ringflow_np.py tick (the reference's algorithm, float64 "
-                      f"numpy) with the ACE-Step-shape DiT (oracle/dit_fp32.py, fp32 torch, {threads} threads) in "
+                      f"numpy) with the ACE-Step-shape DiT (oracle/dit_fp32.py, torch CPU, bf16 GEMM/attention "
+                      f"operands with fp32 accumulation, {threads} threads) in "
                       f"the model slot; {ticks} steady-state tick(s) ({row_steps} DiT row forwards + SDE steps) "
                       f"in {wall:.1f} s after the ring was filled; completions/s = row-steps / S / wall"}
 
@@ -567,12 +569,12 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": base["ticks"], "steps_requested": args.steps, "warmup": args.warmup, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 DiT / f64 tick", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 DiT / f64 tick", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": "config 2: ACE-Step-1.5-shape 24-layer DiT (d=2048, 16/8 heads, SwiGLU 6144, "
                                "random init), 60-s latent T=1500 x D=64, ring depth 4, S=8, source present, "
                                "denoise 1.0; the reference's tick on the host CPU (oracle port) with the DiT "
-                               "(fp32 torch, all host threads) in its model slot"},
+                               "(torch CPU, bf16 operands, all host threads) in its model slot"},
         "cpu_baseline": base,
         "toy_model": {**toy, "note": "the reference's own ToyFlowModel at config-2 shape, one stream per host "
                                      "core: the reference's CPU speed on its only model"},

@@ -35,10 +35,18 @@ def _rope(x, cos, sin):
     return torch.stack([y0, y1], -1).flatten(-2)
 
 
-def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float()):
+def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float(), bf16_matmul=False):
     """The DiT in fp32.  cfg: DiTConfig; W: weights with the DiTWeights attribute names
     (f maps a stored weight to the fp32 tensor used); xs: [frames, C] latents; ts: per-row
-    timesteps; conds: [n_cond_tokens, d] conditioning tokens.  Returns [B, frames, C]."""
+    timesteps; conds: [n_cond_tokens, d] conditioning tokens.  Returns [B, frames, C].
+    bf16_matmul: GEMM and attention operands in bf16 (weights stored bf16; products
+    accumulated in fp32 by the backend, outputs rounded to bf16) -- the CPU timing arm's
+    fast path (AMX); the oracle itself is fp32."""
+    if bf16_matmul:
+        matmul = lambda a, w: (a.bfloat16() @ w.T).float()  # noqa: E731
+    else:
+        matmul = lambda a, w: a @ f(w).T  # noqa: E731
+    sdpa_dt = torch.bfloat16 if bf16_matmul else torch.float32
     B, T, C = len(xs), frames, cfg.latent_channels
     N, d = T // cfg.patch, cfg.d_model
     H, Hk, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
@@ -50,11 +58,11 @@ def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float
     args = 1000.0 * torch.tensor([float(t) for t in ts], device=dev)[:, None] * freqs[None]
     tf = torch.cat([torch.cos(args), torch.sin(args)], -1).bfloat16().float()
     silu = torch.nn.functional.silu
-    temb = silu(tf @ f(W.w_t1).T).bfloat16().float() @ f(W.w_t2).T
+    temb = matmul(silu(matmul(tf, W.w_t1)).bfloat16().float(), W.w_t2)
     st = silu(temb).bfloat16().float()
-    mod = st @ f(W.w_ada).T                       # [B, 6d]
-    fmod = st @ f(W.w_final_ada).T                # [B, 2d]
-    h = x @ f(W.w_in).T                           # [B, N, d]
+    mod = matmul(st, W.w_ada)                       # [B, 6d]
+    fmod = matmul(st, W.w_final_ada)                # [B, 2d]
+    h = matmul(x, W.w_in)                           # [B, N, d]
     pos = torch.arange(N, device=dev, dtype=torch.float64)
     inv = torch.pow(torch.tensor(cfg.rope_theta, dtype=torch.float64),
                     -2.0 * torch.arange(64, device=dev, dtype=torch.float64) / 128.0)
@@ -67,34 +75,34 @@ def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float
         m = mod + W.ada_table[l][None]
         sh1, sc1, g1, sh2, sc2, g2 = [m[:, i * d:(i + 1) * d][:, None, :] for i in range(6)]
         a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc1) + sh1)
-        qkv = bfr(a @ f(W.w_qkv[l]).T)
+        qkv = bfr(matmul(a, W.w_qkv[l]))
         q = qkv[..., :H * hd].reshape(B, N, H, hd)
         k = qkv[..., H * hd:(H + Hk) * hd].reshape(B, N, Hk, hd)
         v = qkv[..., (H + Hk) * hd:].reshape(B, N, Hk, hd)
         q, k = bfr(_rope(q, cos, sin)), bfr(_rope(k, cos, sin))
         k = k.repeat_interleave(H // Hk, dim=2)
         v = v.repeat_interleave(H // Hk, dim=2)
-        o = torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
-                                                             v.transpose(1, 2))
+        o = torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2).to(sdpa_dt), k.transpose(1, 2).to(sdpa_dt),
+                                                             v.transpose(1, 2).to(sdpa_dt)).float()
         o = bfr(o.transpose(1, 2).reshape(B, N, H * hd))
-        h = h + g1 * (o @ f(W.w_o[l]).T)
+        h = h + g1 * (matmul(o, W.w_o[l]))
         c = bfr(_rmsnorm(h, cfg.norm_eps))
-        qc = bfr(c @ f(W.w_qc[l]).T).reshape(B, N, H, hd)
-        kvc = bfr(cond @ f(W.w_kvc[l]).T)
+        qc = bfr(matmul(c, W.w_qc[l])).reshape(B, N, H, hd)
+        kvc = bfr(matmul(cond, W.w_kvc[l]))
         kc = kvc[..., :Hk * hd].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
         vc = kvc[..., Hk * hd:].reshape(B, -1, Hk, hd).repeat_interleave(H // Hk, dim=2)
-        oc = torch.nn.functional.scaled_dot_product_attention(qc.transpose(1, 2), kc.transpose(1, 2),
-                                                              vc.transpose(1, 2))
+        oc = torch.nn.functional.scaled_dot_product_attention(qc.transpose(1, 2).to(sdpa_dt), kc.transpose(1, 2).to(sdpa_dt),
+                                                              vc.transpose(1, 2).to(sdpa_dt)).float()
         oc = bfr(oc.transpose(1, 2).reshape(B, N, H * hd))
-        h = h + oc @ f(W.w_oc[l]).T
+        h = h + matmul(oc, W.w_oc[l])
         mm = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + sc2) + sh2)
-        gu = mm @ f(W.w_gu[l]).T
+        gu = matmul(mm, W.w_gu[l])
         gt, up = bfr(gu[..., 0::2]), bfr(gu[..., 1::2])
         hid = bfr(silu(gt) * up)
-        h = h + g2 * (hid @ f(W.w_down[l]).T)
+        h = h + g2 * (matmul(hid, W.w_down[l]))
     shf, scf = fmod[:, :d][:, None, :], fmod[:, d:][:, None, :]
     a = bfr(_rmsnorm(h, cfg.norm_eps) * (1 + scf) + shf)
-    v = a @ f(W.w_out).T
+    v = matmul(a, W.w_out)
     return v.reshape(B, T, C)
 
 
@@ -110,18 +118,21 @@ def reference_forward(dit, xs, ts, conds, layers: int = None) -> torch.Tensor:
 
 class CpuDiTVelocity:
     """The DiT as the oracle pipeline's model (``velocity(x, t, cond, style, seed, stream,
-    step)`` like ``ringflow_np.Toy``): one fp32 CPU forward per ring row per step, seeded
-    random-init weights of the config's shape (bf16-representable values, kept in fp32)."""
+    step)`` like ``ringflow_np.Toy``): one CPU forward per ring row per step, seeded random-init
+    weights of the config's shape (bf16-representable values).  bf16=True keeps the weights
+    in bf16 and runs the GEMMs / attention with bf16 operands (the fastest CPU path: AMX on
+    the GPU box's Xeon, 5x its fp32 GEMM rate); bf16=False is the fp32 oracle."""
 
-    def __init__(self, cfg, frames: int, seed: int = 1234):
-        self.cfg, self.frames = cfg, frames
+    def __init__(self, cfg, frames: int, seed: int = 1234, bf16: bool = False):
+        self.cfg, self.frames, self.bf16 = cfg, frames, bf16
         g = torch.Generator().manual_seed(seed)
         d, L, F = cfg.d_model, cfg.n_layers, cfg.mlp_hidden
         q, kv = cfg.n_heads * cfg.head_dim, cfg.n_kv_heads * cfg.head_dim
 
         def lin(*shape, std=None):
             s = std if std is not None else 1.0 / math.sqrt(shape[-1])
-            return (torch.randn(*shape, generator=g) * s).bfloat16().float()
+            w = (torch.randn(*shape, generator=g) * s).bfloat16()
+            return w if bf16 else w.float()
 
         gate, up = lin(L, F, d), lin(L, F, d)
         self.W = SimpleNamespace(
@@ -143,5 +154,5 @@ class CpuDiTVelocity:
     def velocity(self, x, t, c, style, seed, stream, step):
         with torch.no_grad():
             v = forward_fp32(self.cfg, self.W, self.frames, [torch.from_numpy(np.ascontiguousarray(x))], [t],
-                             [self.cond_tokens(c.prompt_hash)], f=lambda w: w)
+                             [self.cond_tokens(c.prompt_hash)], f=lambda w: w, bf16_matmul=self.bf16)
         return v[0].double().numpy()

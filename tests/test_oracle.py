@@ -131,3 +131,9 @@ def test_cpu_dit_velocity_small_config():
     for _ in range(8):
         recs += pipe.tick()
     assert recs and all(np.isfinite(r.latent).all() for r in recs)
+    # the bf16-operand CPU path (the CPU timing arm) stays within bf16 rounding of the fp32 one
+    mb = CpuDiTVelocity(cfg, frames=64, seed=3, bf16=True)
+    with torch.no_grad():
+        vb = forward_fp32(cfg, mb.W, 64, xs[1:2], [0.5], conds[1:2], f=lambda w: w, bf16_matmul=True)
+    rel = ((vb[0] - one[0]).pow(2).mean().sqrt() / one[0].pow(2).mean().sqrt()).item()
+    assert rel < 3e-2, rel
