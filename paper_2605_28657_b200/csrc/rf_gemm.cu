@@ -91,8 +91,10 @@ static int launch(const GemmPlan &p, const gemm::EpiArgs &e, cudaStream_t st) {
     return RF_OK;
 }
 
-static bool resid_two_pass() {   // RF_RESID_CC=64: two-pass residual epilogue at every K (tuning aid)
-    static const bool v = getenv("RF_RESID_CC") && atoi(getenv("RF_RESID_CC")) == 64;
+// Tuning aid: RF_RESID_CC=64 stages the residual in two 64-column passes at every K,
+// RF_RESID_CC=128 in one pass at every K (default: two passes only for K >= 4096).
+static int resid_cc_override() {
+    static const int v = getenv("RF_RESID_CC") ? atoi(getenv("RF_RESID_CC")) : 0;
     return v;
 }
 
@@ -107,7 +109,8 @@ static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStre
             if constexpr (BN == 256) {
                 return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
             } else {
-                if (p.K >= 4096 || resid_two_pass()) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
+                const int cc = resid_cc_override();
+                if (cc == 64 || (cc != 128 && p.K >= 4096)) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
                 return launch<BN, gemm::kResidGate, CG>(p, e, st);
             }
         case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG>(p, e, st);
