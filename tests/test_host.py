@@ -122,3 +122,28 @@ def test_config_and_request_validation():
     assert a.content_key() == b.content_key()
     r = rf.GenerationRequest(conditions=(a,), solver="ode")
     assert r.content_key() == O.Request([b], solver="ode").content_key()
+
+
+def test_bench_reference_arm_json_contract():
+    """`bench.py --impl reference` (the CPU arm the driver runs): one JSON line on the same
+    metric / unit as our arm, impl "reference", a cpu_baseline describing the run and an e2e
+    object with zero host<->device bytes; the sample is the config-2 workload (DiT in the
+    reference tick's model slot) and the reference's toy model is reported beside it."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    import bench
+
+    assert line["impl"] == "reference" and line["metric"] == bench.METRIC and line["unit"] == bench.UNIT
+    assert line["higher_is_better"] is True and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["cpu_baseline"]["ticks"] >= 1 and "DiT" in line["cpu_baseline"]["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": bench.UNIT, "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert line["toy_model"]["value"] > 0
