@@ -8,8 +8,12 @@
 //   * Layer l: CTA r computes output channels [r*C/NC, (r+1)*C/NC) for the frames whose
 //     taps stay inside the staged region (the region shrinks by d_l per side), with
 //     its slice of the conv weights resident in shared memory.  Each output is a
-//     fixed-order sum (4 lanes x C/4 input channels x 3 taps, fixed shuffle tree), tanh,
-//     and zero outside [vlo, vhi).
+//     fixed-order sum (8 lanes x C/8 input channels x 3 taps, fixed shuffle tree), tanh,
+//     and zero outside [vlo, vhi).  A group of 8 lanes computes all of the CTA's C/NC
+//     channels of one frame: every activation load feeds C/NC independent FMA chains, the
+//     weights are stored [tap][k/8][channel][k%8] so the 8 lanes read consecutive doubles,
+//     activation rows are padded by 8 doubles (two groups' rows fall on different banks),
+//     and after the reduction tree lane j applies tanh to channel j.
 //   * After each layer the cluster synchronises and every CTA gathers the other CTAs'
 //     channel slices through distributed shared memory (DSMEM), so activations never
 //     leave the SMs.
@@ -61,15 +65,16 @@ __global__ void __launch_bounds__(kThreads)
 rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
     constexpr int CS = C / kNC;       // output channels per CTA
     constexpr int KPER = C / kKS;     // input channels per lane of a conv output
+    constexpr int ACS = C + 8;        // padded activation row (bank spread across frame rows)
     extern __shared__ __align__(16) double sm[];
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     const int L = A.L;
     const int W = kTF + 2 * A.rf;
     const int jper = (int)((A.hop + kNC - 1) / kNC);
-    double *act = sm;                                   // [W][C]   current layer input
-    double *part0 = act + (size_t)W * C;                // [2][W][CS] this CTA's layer output
-    double *wts = part0 + (size_t)2 * W * CS;           // [L][3][C][CS]
+    double *act = sm;                                   // [W][ACS] current layer input
+    double *part0 = act + (size_t)W * ACS;              // [2][W][CS] this CTA's layer output
+    double *wts = part0 + (size_t)2 * W * CS;           // [L][3][C/8][CS][8] (tap, k/8, out, k%8)
     double *hT = wts + (size_t)L * 3 * C * CS;          // [C][kTF] final layer, transposed
     double *ups = hT + (size_t)C * kTF;                 // [C][jper] this CTA's U^T slice
     const int64_t tile = blockIdx.x / kNC;
@@ -84,13 +89,15 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
         const int c = threadIdx.x % C;
         const int64_t g = gbase + w;
         const bool in = g >= A.vlo && g < A.vhi;
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(act + w * C + c);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(act + w * ACS + c);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst),
                      "l"(A.latent + (in ? g * C + c : 0)), "r"(in ? 8 : 0));
     }
     for (int rest = threadIdx.x / CS; rest < L * 3 * C; rest += kThreads / CS) {
         const int cc = threadIdx.x % CS;                // rest = (l*3 + tap)*C + k
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(wts + rest * CS + cc);
+        const int lt = rest / C, k = rest % C;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(
+            wts + (((size_t)lt * KPER + k / kKS) * CS + cc) * kKS + k % kKS);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
                      "l"(A.kernels + (int64_t)rest * C + c0 + cc));
     }
@@ -115,36 +122,49 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
         const int d = A.dil[l];
         const int olo = lo + d, ohi = hi - d;
         const double *K = wts + (size_t)l * 3 * C * CS;
-        const int nout = (ohi - olo) * CS;
+        const int nf = ohi - olo;                             // frames of this layer
         double *part = part0 + (size_t)(l & 1) * W * CS;  // double-buffered across layers
-        for (int base = 0; base < nout; base += ngrp) {
-            const int o = base + grp;
-            const bool live = o < nout;
-            const int w = live ? olo + o / CS : olo;
-            const int cc = live ? o % CS : 0;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int base = 0; base < nf; base += ngrp) {
+            const int fi = base + grp;
+            const bool live = fi < nf;
+            const int w = live ? olo + fi : olo;
+            double s0[CS], s1[CS], s2[CS];
+#pragma unroll
+            for (int cc = 0; cc < CS; ++cc) s0[cc] = s1[cc] = s2[cc] = 0.0;
             if (live) {
-                // lane `sub` takes input channels sub, sub+8, ... so the 8 lanes of a
-                // group read consecutive doubles of both operands (no bank conflicts)
-                const double *r0 = act + (w - d) * C + sub;
-                const double *r1 = act + w * C + sub;
-                const double *r2 = act + (w + d) * C + sub;
-                const double *kk = K + sub * CS + cc;
+                // lane `sub` takes input channels sub, sub+8, ...: the 8 lanes of a group
+                // read consecutive doubles of the activations and of the weights
+                const double *r0 = act + (w - d) * ACS + sub;
+                const double *r1 = act + w * ACS + sub;
+                const double *r2 = act + (w + d) * ACS + sub;
+                const double *kk = K + sub;
 #pragma unroll
                 for (int k = 0; k < KPER; ++k) {
-                    s0 = fma(r0[k * kKS], kk[(0 * C + k * kKS) * CS], s0);
-                    s1 = fma(r1[k * kKS], kk[(1 * C + k * kKS) * CS], s1);
-                    s2 = fma(r2[k * kKS], kk[(2 * C + k * kKS) * CS], s2);
+                    const double a0 = r0[k * kKS], a1 = r1[k * kKS], a2 = r2[k * kKS];
+                    const double *k0 = kk + ((0 * KPER + k) * CS) * kKS;
+                    const double *k1 = kk + ((1 * KPER + k) * CS) * kKS;
+                    const double *k2 = kk + ((2 * KPER + k) * CS) * kKS;
+#pragma unroll
+                    for (int cc = 0; cc < CS; ++cc) {
+                        s0[cc] = fma(a0, k0[cc * kKS], s0[cc]);
+                        s1[cc] = fma(a1, k1[cc * kKS], s1[cc]);
+                        s2[cc] = fma(a2, k2[cc * kKS], s2[cc]);
+                    }
                 }
             }
-            double s = __dadd_rn(__dadd_rn(s0, s1), s2);
-            // fixed 8-lane reduction tree (the lanes of a group are adjacent)
-            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
-            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
-            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-            if (live && sub == 0) {
+            double mine = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < CS; ++cc) {
+                double s = __dadd_rn(__dadd_rn(s0[cc], s1[cc]), s2[cc]);
+                // fixed 8-lane reduction tree (the lanes of a group are adjacent)
+                s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+                s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+                s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+                if (cc == sub % CS) mine = s;
+            }
+            if (live && sub < CS) {   // lane j: channel j (tanh spread over the group)
                 const int64_t g = gbase + w;
-                part[w * CS + cc] = (g >= A.vlo && g < A.vhi) ? tanh(s) : 0.0;
+                part[w * CS + sub] = (g >= A.vlo && g < A.vhi) ? tanh(mine) : 0.0;
             }
         }
         cluster.sync();   // every CTA's slice of layer l is complete (and, because each
@@ -169,7 +189,7 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
                     if (last)
                         hT[c * kTF + (w - olo)] = v[u];
                     else
-                        act[w * C + c] = v[u];
+                        act[w * ACS + c] = v[u];
                 }
             }
         }
@@ -269,7 +289,7 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
     A.out = out;
     const int W = kTF + 2 * rfield;
     const int64_t jper = (hop + kNC - 1) / kNC;
-    size_t smem = ((size_t)W * channels + (size_t)2 * W * A.CS + (size_t)n_layers * 3 * channels * A.CS +
+    size_t smem = ((size_t)W * (channels + 8) + (size_t)2 * W * A.CS + (size_t)n_layers * 3 * channels * A.CS +
                    (size_t)channels * kTF + (size_t)channels * jper) * sizeof(double);
     if (smem > 220 * 1024) {
         set_error("rf_decode_window: receptive field / hop too large for one tile (%zu B smem)", smem);
