@@ -85,13 +85,15 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
     // All staging is asynchronous (cp.async, 8-byte granules, zero-fill outside the
     // valid frame range): the tile + halo and the weight slice in group 0, this CTA's
     // upsampler slice in group 1, which is only waited for after the conv layers.
-    for (int w = threadIdx.x / C; w < W; w += kThreads / C) {
-        const int c = threadIdx.x % C;
+    // (16-byte granules: a frame row of C doubles is 16-byte aligned in both spaces)
+    constexpr int C2 = C / 2;
+    for (int w = threadIdx.x / C2; w < W; w += kThreads / C2) {
+        const int c = 2 * (threadIdx.x % C2);
         const int64_t g = gbase + w;
         const bool in = g >= A.vlo && g < A.vhi;
         const unsigned dst = (unsigned)__cvta_generic_to_shared(act + w * ACS + c);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst),
-                     "l"(A.latent + (in ? g * C + c : 0)), "r"(in ? 8 : 0));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst),
+                     "l"(A.latent + (in ? g * C + c : 0)), "r"(in ? 16 : 0));
     }
     for (int rest = threadIdx.x / CS; rest < L * 3 * C; rest += kThreads / CS) {
         const int cc = threadIdx.x % CS;                // rest = (l*3 + tap)*C + k
@@ -104,9 +106,17 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
     asm volatile("cp.async.commit_group;\n" ::);
     const int j0 = rank * jper;
     const int jn = (int)(j0 + jper < A.hop ? jper : A.hop - j0);
-    for (int c = 0; c < C; ++c) {
+    // U^T slice: 16-byte granules when both row starts are 16-byte aligned (hop, jper even)
+    const bool up16 = ((A.hop | jper | j0) & 1) == 0;
+    const int jq = up16 ? (jn + 1) / 2 : jn;   // granules per row
+    for (int e = threadIdx.x; e < C * jq; e += kThreads) {
+        const int c = e / jq, q = e % jq;
         const double *src = A.upT + (int64_t)c * A.hop + j0;
-        for (int jj = threadIdx.x; jj < jn; jj += kThreads) {
+        if (up16 && 2 * q + 1 < jn) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(ups + (size_t)c * jper + 2 * q);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + 2 * q));
+        } else {
+            const int jj = up16 ? 2 * q : q;
             const unsigned dst = (unsigned)__cvta_generic_to_shared(ups + (size_t)c * jper + jj);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src + jj));
         }
