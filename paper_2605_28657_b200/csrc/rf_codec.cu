@@ -33,7 +33,8 @@ namespace cg = cooperative_groups;
 namespace rf {
 
 constexpr int kNC = 8;          // CTAs per cluster
-constexpr int kTF = 16;         // output frames per cluster
+// output frames per cluster: 16, or 8 for short windows (twice the clusters: a 3-s window
+// then spreads over 80 instead of 40 SMs; per-frame arithmetic is independent of the tiling)
 constexpr int kThreads = 256;
 constexpr int kKS = 8;          // lanes cooperating on one conv output
 constexpr int kMaxC = 64;
@@ -60,7 +61,7 @@ __device__ __forceinline__ int16_t quantize_pcm(double s) {
     return (int16_t)(int)r;
 }
 
-template <int C>
+template <int C, int kTF>
 __global__ void __launch_bounds__(kThreads)
 rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
     constexpr int CS = C / kNC;       // output channels per CTA
@@ -297,6 +298,8 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
     A.upT = upsample_t;
     A.hop = hop;
     A.out = out;
+    // short outputs: 8-frame tiles (more clusters in flight); long ones: 16 (less halo work)
+    const int kTF = (stop - start) <= 8 * 148 / kNC * 2 ? 8 : 16;
     const int W = kTF + 2 * rfield;
     const int64_t jper = (hop + kNC - 1) / kNC;
     size_t smem = ((size_t)W * (channels + 8) + (size_t)2 * W * A.CS + (size_t)n_layers * 3 * channels * A.CS +
@@ -305,10 +308,13 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
         set_error("rf_decode_window: receptive field / hop too large for one tile (%zu B smem)", smem);
         return RF_EINVAL;
     }
-    void (*kern)(DecodeArgs) = channels == 8    ? rf_decode_cluster<8>
-                               : channels == 16 ? rf_decode_cluster<16>
-                               : channels == 32 ? rf_decode_cluster<32>
-                                                : rf_decode_cluster<64>;
+    void (*kern)(DecodeArgs);
+    if (kTF == 8)
+        kern = channels == 8 ? rf_decode_cluster<8, 8> : channels == 16 ? rf_decode_cluster<16, 8>
+             : channels == 32 ? rf_decode_cluster<32, 8> : rf_decode_cluster<64, 8>;
+    else
+        kern = channels == 8 ? rf_decode_cluster<8, 16> : channels == 16 ? rf_decode_cluster<16, 16>
+             : channels == 32 ? rf_decode_cluster<32, 16> : rf_decode_cluster<64, 16>;
     RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t tiles = (A.nout + kTF - 1) / kTF;
     cudaLaunchConfig_t cfg{};
