@@ -78,24 +78,26 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
     double *wts = part0 + (size_t)2 * W * CS;           // [L][3][C/8][CS][8] (tap, k/8, out, k%8)
     double *hT = wts + (size_t)L * 3 * C * CS;          // [C][kTF] final layer, transposed
     double *ups = hT + (size_t)C * kTF;                 // [C][jper] this CTA's U^T slice
-    const int64_t tile = blockIdx.x / kNC;
-    const int64_t g0 = A.start + tile * kTF;
-    const int64_t gbase = g0 - A.rf;
     const int c0 = rank * CS;
+    // persistent clusters: cluster q decodes tiles q, q + nclusters, ...; the weight and
+    // upsampler slices are staged once per CTA, the latent tile + halo once per tile
+    const int64_t ntiles = (A.nout + kTF - 1) / kTF;
+    const int64_t nclusters = gridDim.x / kNC;
 
-    // All staging is asynchronous (cp.async, 8-byte granules, zero-fill outside the
-    // valid frame range): the tile + halo and the weight slice in group 0, this CTA's
-    // upsampler slice in group 1, which is only waited for after the conv layers.
-    // (16-byte granules: a frame row of C doubles is 16-byte aligned in both spaces)
-    constexpr int C2 = C / 2;
-    for (int w = threadIdx.x / C2; w < W; w += kThreads / C2) {
-        const int c = 2 * (threadIdx.x % C2);
-        const int64_t g = gbase + w;
-        const bool in = g >= A.vlo && g < A.vhi;
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(act + w * ACS + c);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst),
-                     "l"(A.latent + (in ? g * C + c : 0)), "r"(in ? 16 : 0));
-    }
+    // the tile + halo (16-byte cp.async granules, zero-fill outside the valid frame range)
+    auto stage_tile = [&](int64_t gbase) {
+        constexpr int C2 = C / 2;
+        for (int w = threadIdx.x / C2; w < W; w += kThreads / C2) {
+            const int c = 2 * (threadIdx.x % C2);
+            const int64_t g = gbase + w;
+            const bool in = g >= A.vlo && g < A.vhi;
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(act + w * ACS + c);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst),
+                         "l"(A.latent + (in ? g * C + c : 0)), "r"(in ? 16 : 0));
+        }
+    };
+    // Groups: weights + the first tile, then this CTA's upsampler slice, which the first
+    // tile only waits for after its conv layers.
     for (int rest = threadIdx.x / CS; rest < L * 3 * C; rest += kThreads / CS) {
         const int cc = threadIdx.x % CS;                // rest = (l*3 + tap)*C + k
         const int lt = rest / C, k = rest % C;
@@ -104,6 +106,7 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
                      "l"(A.kernels + (int64_t)rest * C + c0 + cc));
     }
+    if (blockIdx.x / kNC < ntiles) stage_tile(A.start + (blockIdx.x / kNC) * kTF - A.rf);
     asm volatile("cp.async.commit_group;\n" ::);
     const int j0 = rank * jper;
     const int jn = (int)(j0 + jper < A.hop ? jper : A.hop - j0);
@@ -123,7 +126,17 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
         }
     }
     asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 1;\n" ::);
+  bool first = true;
+  for (int64_t tile = blockIdx.x / kNC; tile < ntiles; tile += nclusters) {
+    const int64_t g0 = A.start + tile * kTF;
+    const int64_t gbase = g0 - A.rf;
+    if (!first) {
+        stage_tile(gbase);
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_all;\n" ::);
+    } else {
+        asm volatile("cp.async.wait_group 1;\n" ::);   // weights + first tile; U^T may still fly
+    }
     __syncthreads();
 
     const int grp = threadIdx.x / kKS, sub = threadIdx.x % kKS;
@@ -208,9 +221,12 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
         lo = olo;
         hi = ohi;
     }
-    cluster.sync();   // no CTA may exit while a peer could still read its `part`
-    asm volatile("cp.async.wait_all;\n" ::);
-    __syncthreads();
+    cluster.sync();   // no CTA may exit (or restage) while a peer could still read its `part`
+    if (first) {
+        asm volatile("cp.async.wait_all;\n" ::);   // the upsampler slice
+        __syncthreads();
+        first = false;
+    }
     // pcm[f][j] = quantize(sum_c h[f][c] U[j][c]) for this CTA's samples
     const int64_t fmax = A.nout - tile * kTF < kTF ? A.nout - tile * kTF : kTF;
     for (int jj = threadIdx.x; jj < jn; jj += kThreads) {
@@ -233,6 +249,8 @@ rf_decode_cluster(const __grid_constant__ DecodeArgs A) {
         for (int f = 0; f < kTF; ++f)
             if (f < fmax) A.out[(tile * kTF + f) * A.hop + j] = quantize_pcm(acc[f]);
     }
+    __syncthreads();   // hT and act are read before the next tile overwrites them
+  }
 }
 
 }  // namespace rf
@@ -318,7 +336,6 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
     RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t tiles = (A.nout + kTF - 1) / kTF;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(tiles * kNC));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = (cudaStream_t)stream;
@@ -329,6 +346,17 @@ extern "C" int rf_decode_window(const double *latent, int64_t frames, int64_t ch
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // persistent: as many clusters as can be co-resident (8-CTA clusters must fit in one
+    // GPC, so this is below sm_count / 8); a non-resident cluster would run its whole tile
+    // list after the others
+    int active = 0;
+    cfg.gridDim = dim3((unsigned)kNC);
+    if (cudaOccupancyMaxActiveClusters(&active, (void *)kern, &cfg) != cudaSuccess || active < 1) {
+        cudaGetLastError();
+        active = 1;
+    }
+    const int64_t clusters = tiles < active ? tiles : active;
+    cfg.gridDim = dim3((unsigned)(clusters * kNC));
     RF_TRY_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     return RF_OK;
 }
