@@ -46,9 +46,15 @@ static int make_tmap_2d(CUtensorMap *map, CUtensorMapDataType dt, const void *pt
     cuuint64_t strides[1] = {row_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t es[2] = {1, 1};
+    // L2 promotion of the TMA fetches (tuning aid RF_TMA_L2PROMO = 0 / 64 / 128 / 256; default 256)
+    static const int promo = getenv("RF_TMA_L2PROMO") ? atoi(getenv("RF_TMA_L2PROMO")) : 256;
+    const CUtensorMapL2promotion pr = promo == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                      : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                      : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     CUresult r = enc(map, dt, 2, const_cast<void *>(ptr), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d) inner=%llu outer=%llu stride=%llu", (int)r,
                   (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_bytes);
