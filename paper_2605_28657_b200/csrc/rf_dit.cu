@@ -324,9 +324,20 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     // cross-Q projection + cross-attention epilogue on CTA pairs (256-row tiles, cta_group::2
     // attention MMAs); RF_DIT_XATT_PAIR=0 keeps single-CTA 128-row tiles (A/B timing)
     const int xattn_cg = (getenv("RF_DIT_XATT_PAIR") && atoi(getenv("RF_DIT_XATT_PAIR")) == 0) ? 1 : 2;
+    const int qkv_bn = getenv("RF_DIT_QKV_BN") ? atoi(getenv("RF_DIT_QKV_BN")) : 0;
+    // tuning aid RF_DIT_PROJ_BN=256: the N = d_model projections (O, cross-O, down) on
+    // 256 x 256 pair tiles instead of 256 x 128
+    const int proj_bn = getenv("RF_DIT_PROJ_BN") ? atoi(getenv("RF_DIT_PROJ_BN")) : 0;
+
     int rc = 0;
     auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
         if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N), M >= 1024 ? 2 : 1);
+    };
+    auto plan_proj = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
+        if (proj_bn && !rc)
+            rc = gemm_plan(p, A, Bw, M, N, K, K, K, proj_bn, M >= 1024 ? 2 : 1);
+        else
+            plan(p, A, Bw, M, N, K);
     };
     plan(&d->p_in, d->xin, w->w_in, BN, D, d->in_dim);
     plan(&d->p_t1, d->tfeat, w->w_t1, Bmax, D, c.freq_dim);
@@ -346,16 +357,20 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     const __nv_bfloat16 *woc = (const __nv_bfloat16 *)w->w_oc, *wgu = (const __nv_bfloat16 *)w->w_gu;
     const __nv_bfloat16 *wdn = (const __nv_bfloat16 *)w->w_down;
     for (int64_t l = 0; l < L; ++l) {
-        plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
-        plan(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
+        if (qkv_bn)   // tuning aid RF_DIT_QKV_BN=128|256 (default: bn_for)
+            rc = rc ? rc : gemm_plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D, D, D, qkv_bn,
+                                     BN >= 1024 ? 2 : 1);
+        else
+            plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
+        plan_proj(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_qc[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D);
         if (!rc) rc = gemm_plan(&d->p_qcx[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D, D, D, 128, xattn_cg);
-        plan(&d->p_oc[l], d->att, woc + l * D * d->q_dim, BN, D, d->q_dim);
+        plan_proj(&d->p_oc[l], d->att, woc + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_gu[l], d->a, wgu + l * 2 * (int64_t)c.mlp_hidden * D, BN, 2 * (int64_t)c.mlp_hidden, D);
-        plan(&d->p_down[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, BN, D, c.mlp_hidden);
+        plan_proj(&d->p_down[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, BN, D, c.mlp_hidden);
         // gated-residual outputs all update h: bind it once (TMA map of the epilogue)
         for (GemmPlan *g : {&d->p_o[l], &d->p_oc[l], &d->p_down[l]})
-            if (!rc && g->bn == 128) rc = gemm_plan_c(g, d->h, D);
+            if (!rc) rc = gemm_plan_c(g, d->h, D);
         if (!rc && d->p_gu[l].bn == 256) rc = gemm_plan_o(&d->p_gu[l], d->mlp, c.mlp_hidden);
     }
     // the cross-attention K/V projections of all layers read the same conditioning tokens:
@@ -497,7 +512,7 @@ static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) 
             nf_out.sq_ld = BNmax;
             nf_in.rs_part = d.sq_part;
             nf_in.rs_ld = BNmax;
-            nf_in.rs_tiles = (int)(D / 128);
+            nf_in.rs_tiles = (int)(D / d.p_o[l].bn);   // one partial sum per O-projection tile column
             nf_in.rs_inv_d = 1.0f / (float)D;
             nf_in.rs_eps = c.norm_eps;
         }
