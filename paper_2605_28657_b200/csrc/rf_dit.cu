@@ -38,13 +38,13 @@ constexpr int kMaxDitRows = 64;
 // RMSNorm over d (fp32 residual row) with optional AdaLN modulation, bf16 out.
 // One warp per token row; shift/scale are indexed by the row's batch entry.
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
 rf_dit_norm_mod(const float *__restrict__ h, int64_t rows, int tokens, const float *__restrict__ shift,
                 const float *__restrict__ scale, int64_t mod_ld, __nv_bfloat16 *__restrict__ out, float eps) {
     pdl_wait();
     pdl_launch();
     constexpr int PER = D / 32 / 4;  // float4 per lane
-    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
     const float4 *x = (const float4 *)(h + row * D);
@@ -430,12 +430,14 @@ extern "C" int rf_dit_destroy(void *handle) {
 
 static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shift, const float *scale,
                     int64_t mod_ld, __nv_bfloat16 *out, cudaStream_t st) {
-    const unsigned blocks = (unsigned)((rows + 7) / 8);
+    // rows (warps) per block: 8 (tuning aid RF_DIT_NORM_ROWS = 4 / 8 / 16)
+    static const int rpb = getenv("RF_DIT_NORM_ROWS") ? atoi(getenv("RF_DIT_NORM_ROWS")) : 8;
+    const unsigned blocks = (unsigned)((rows + rpb - 1) / rpb);
     switch (d.c.d_model) {
-        case 2048: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<2048>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
-        case 1024: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<1024>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
-        case 512: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<512>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
-        default: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<256>, dim3(blocks), dim3(256), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
+        case 2048: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<2048>, dim3(blocks), dim3(32 * rpb), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
+        case 1024: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<1024>, dim3(blocks), dim3(32 * rpb), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
+        case 512: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<512>, dim3(blocks), dim3(32 * rpb), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
+        default: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<256>, dim3(blocks), dim3(32 * rpb), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
     }
     RF_TRY_LAUNCH("rf_dit_norm_mod");
     return RF_OK;
