@@ -16,8 +16,8 @@ the ring completes one generation every 2 ticks.
               only model the reference has); compare with cpu_baseline_toy_model
   cpu_baseline / --impl reference = the same config-2 workload on the host CPU: the
               reference's tick (oracle port, float64 numpy) with the DiT (oracle/dit_fp32.py,
-              fp32 torch on all host threads) in its model slot; the reference arm also
-              reports the reference's toy model on all cores (`toy_model`)
+              torch CPU, bf16 GEMM/attention operands, all host threads) in its model slot;
+              the reference arm also reports the reference's toy model on all cores (`toy_model`)
   library_baseline = the same DiT forward in stock PyTorch (cuBLAS + SDPA) on the GPU
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
