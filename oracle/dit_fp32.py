@@ -9,10 +9,11 @@ import this module; the product package (paper_2605_28657_b200/) never does.
   no DiT, so DiT parity is unpinned by it; this is the oracle the GPU
   forward is tested against (tests/test_gpu_dit.py, rel-RMS tolerance stated there).
 * ``reference_forward(dit, ...)`` -- the same on a GPU ``DiT``'s own weights.
-* ``CpuDiTVelocity`` -- the network on the host CPU with fp32 weights, plugged into the
-  oracle pipeline's model slot (``oracle/ringflow_np.py``: ``Pipeline.model.velocity``) so
-  bench.py can time the reference's CPU path at config 2 on the same workload as the GPU
-  arm (a DiT forward per ring row per tick), not the toy model.
+* ``CpuDiTVelocity`` -- the network on the host CPU (fp32, or bf16 GEMM / attention operands
+  for the timing arm), plugged into the oracle pipeline's model slot
+  (``oracle/ringflow_np.py``: ``Pipeline.model.velocity``) so bench.py can time the
+  reference's CPU path at config 2 on the same workload as the GPU arm (a DiT forward per
+  ring row per tick), not the toy model.
 """
 from __future__ import annotations
 
