@@ -325,6 +325,11 @@ def run_ours(args):
     model = dit_mod.DiT(dcfg, frames=T, max_rows=DEPTH)
     pipe = rf.StreamPipeline(conf, request=make_request(rf, rank), velocity_model=dit_mod.DiTVelocity(model))
     st = pipe.stream
+    # setup: fill the ring (warmup pacing admits one slot per ceil(S/D) ticks) until the first
+    # generation completes -- the steady state every timed tick is in; then W warm-up ticks
+    fill = 0
+    while fill < 4 * STEPS and not pipe.tick():
+        fill += 1
     for _ in range(args.warmup):
         pipe.tick()
     torch.cuda.synchronize()
