@@ -330,8 +330,11 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     const int proj_bn = getenv("RF_DIT_PROJ_BN") ? atoi(getenv("RF_DIT_PROJ_BN")) : 0;
 
     int rc = 0;
+    // CTA pairs from this many rows up (tuning aid RF_DIT_PAIR_MIN_M; the all-layer cross K/V
+    // projection has max_rows x n_cond_tokens rows)
+    const int64_t pair_min_m = getenv("RF_DIT_PAIR_MIN_M") ? atoll(getenv("RF_DIT_PAIR_MIN_M")) : 1024;
     auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
-        if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N), M >= 1024 ? 2 : 1);
+        if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N), M >= pair_min_m ? 2 : 1);
     };
     auto plan_proj = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
         if (proj_bn && !rc)
