@@ -588,7 +588,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def refuse_tuning_env():
+    """The product library reads no environment knobs; refuse to time a run that sets RF_*
+    variables anyway (a leftover from an experiment must not leak into a bench number)."""
+    bad = sorted(k for k in os.environ if k.startswith("RF_"))
+    if bad:
+        sys.exit(f"bench.py: refusing to run with RF_* environment variables set: {bad}")
+
+
 if __name__ == "__main__":
+    refuse_tuning_env()
     a = parse()
     if a.impl == "reference":
         run_reference(a)

@@ -121,6 +121,9 @@ typedef struct rf_row {
 #define RF_ROWF_UNCOND_V 0x20      /* uncond_x0 holds the negative velocity */
 #define RF_ROWF_NO_STEP 0x40       /* velocity only (guided_velocity seam): x untouched */
 #define RF_ROWF_V_F32 0x80         /* cond/uncond velocities are float32 (DiT output) */
+#define RF_ROWF_STYLE_V 0x100      /* given velocities get the shared style offset applied in
+                                      x0 space: v' = v - style/t_curr (model.py:123-131's
+                                      x0 + style_offset for a velocity-predicting model) */
 
 /* rows: HOST array of `count` rows; style_offset: device [T*D] (ModelWeights). */
 int rf_tick_solve(const rf_row *rows, int count, int64_t frames, int64_t channels,
@@ -148,14 +151,19 @@ int rf_x0_compose(double *out, const double *base, const double *hint, double hs
  * its record buffer, flag non-finite values, and compute
  *   mse_prev[e] = mean((lat_e - prev_e)^2), prev_e = lat_{e-1} (or `last` for e = 0)
  *   mse_ref[e]  = mean((lat_e - reference)^2)
- * with a fixed-order (deterministic) reduction.  `prev`/`reference` may be NULL. */
+ * with a fixed-order (deterministic) reduction.  `prev`/`reference` may be NULL.
+ * Any count: emits run in launches of 16, each chunk's first prev being the previous
+ * chunk's last latent.  scratch: device doubles owned by the caller (one buffer per
+ * stream), at least rf_reduce_workspace_elems(numel). */
 typedef struct rf_emit {
     const double *latent; /* slot state */
     double *record;       /* record-owned copy */
 } rf_emit;
 int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, const double *last,
                   const double *reference, double *mse_prev, double *mse_ref,
-                  uint32_t *status, void *stream);
+                  uint32_t *status, double *scratch, int64_t scratch_elems, void *stream);
+/* Scratch doubles rf_emit_stats / rf_mse need for latents of `numel` elements. */
+int64_t rf_reduce_workspace_elems(int64_t numel);
 
 /* ------------------------------------------------------------- codec (B1-B9) -----
  * ToyCodec (codec.py:67-174).  The decode of an extended window [F, C] runs the
@@ -202,15 +210,11 @@ int rf_gemm_bf16(const void *A, const void *B, void *out, int64_t M, int64_t N, 
                  int64_t ldb, int64_t ldo, int32_t epilogue, const float *gate, int64_t gate_ld,
                  int32_t rows_per_batch, float alpha, int32_t block_n, void *stream);
 
-/* Multi-head attention (flash schedule, bf16 in/out, fp32 softmax), head_dim 128:
- * q [batch*n_q, ldq] (head h at column h*128), k/v [batch*n_k, ld] with kv head
- * h / (heads / kv_heads); out [batch*n_q, ldo]. */
-int rf_attention_bf16(const void *q, const void *k, const void *v, void *out, int32_t batch, int32_t n_q,
-                      int32_t n_k, int32_t heads, int32_t kv_heads, int64_t ldq, int64_t ldk, int64_t ldv,
-                      int64_t ldo, void *stream);
-
-/* Same attention on tcgen05/TMEM (two-pass softmax, O accumulated in TMEM); V is given
- * transposed: vt [batch, kv_heads, 128, n_k_pad] (keys contiguous, pad columns zero). */
+/* Multi-head attention on tcgen05/TMEM (single-pass online softmax, bf16 in/out, fp32
+ * softmax and accumulation), head_dim 128: q [batch*n_q, ldq] (head h at column h*128),
+ * k [batch*n_k, ldk] with kv head h / (heads / kv_heads); V is given transposed:
+ * vt [batch, kv_heads, 128, n_k_pad] (keys contiguous, pad columns zero);
+ * out [batch*n_q, ldo]. */
 int rf_attention_tc_bf16(const void *q, const void *k, const void *vt, void *out, int32_t batch, int32_t n_q,
                          int32_t n_k, int32_t n_k_pad, int32_t heads, int32_t kv_heads, int64_t ldq, int64_t ldk,
                          int64_t ldo, void *stream);
@@ -264,8 +268,9 @@ int rf_dit_forward(void *handle, int32_t rows, const double *const *x_rows, cons
                    const void *const *cond_rows, float *v_out, void *stream);
 float *rf_dit_output(void *handle);
 
-/* Squared-difference reductions used by the similarity filter and tests. */
-int rf_mse(const double *a, const double *b, int64_t numel, double *out, void *stream);
+/* Squared-difference reduction used by the similarity filter and tests (fixed order). */
+int rf_mse(const double *a, const double *b, int64_t numel, double *out, double *scratch,
+           int64_t scratch_elems, void *stream);
 
 #ifdef __cplusplus
 }

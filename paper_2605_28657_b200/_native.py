@@ -38,6 +38,7 @@ RF_ROWF_COND_V = 0x10
 RF_ROWF_UNCOND_V = 0x20
 RF_ROWF_NO_STEP = 0x40
 RF_ROWF_V_F32 = 0x80
+RF_ROWF_STYLE_V = 0x100
 
 c_dptr = ctypes.c_void_p
 
@@ -84,9 +85,9 @@ class RfEmit(ctypes.Structure):
 EXPORTS = (
     "rf_abi_version", "rf_last_error", "rf_device_sm_count",
     "rf_normal_workspace_bytes", "rf_normal_fill", "rf_uniform_fill",
-    "rf_tick_solve", "rf_x0_compose", "rf_admit_init", "rf_emit_stats",
+    "rf_tick_solve", "rf_x0_compose", "rf_admit_init", "rf_emit_stats", "rf_reduce_workspace_elems",
     "rf_decode_workspace_bytes", "rf_decode_window", "rf_encode_frames", "rf_mse", "rf_gemm_bf16",
-    "rf_attention_bf16", "rf_dit_workspace_bytes", "rf_dit_create", "rf_dit_destroy", "rf_dit_forward",
+    "rf_dit_workspace_bytes", "rf_dit_create", "rf_dit_destroy", "rf_dit_forward",
     "rf_dit_output", "rf_attention_tc_bf16",
 )
 
@@ -143,7 +144,9 @@ def _declare(lib):
     lib.rf_admit_init.restype = i32
     lib.rf_admit_init.argtypes = [ctypes.POINTER(RfAdmit), i32, i64, vp]
     lib.rf_emit_stats.restype = i32
-    lib.rf_emit_stats.argtypes = [ctypes.POINTER(RfEmit), i32, i64, vp, vp, vp, vp, u32p, vp]
+    lib.rf_emit_stats.argtypes = [ctypes.POINTER(RfEmit), i32, i64, vp, vp, vp, vp, u32p, vp, i64, vp]
+    lib.rf_reduce_workspace_elems.restype = i64
+    lib.rf_reduce_workspace_elems.argtypes = [i64]
     lib.rf_decode_workspace_bytes.restype = i64
     lib.rf_decode_workspace_bytes.argtypes = [i64, i64]
     lib.rf_decode_window.restype = i32
@@ -155,7 +158,7 @@ def _declare(lib):
     lib.rf_gemm_bf16.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, i64, ctypes.c_int32, vp, i64,
                                  ctypes.c_int32, ctypes.c_float, ctypes.c_int32, vp]
     lib.rf_mse.restype = i32
-    lib.rf_mse.argtypes = [vp, vp, i64, vp, vp]
+    lib.rf_mse.argtypes = [vp, vp, i64, vp, vp, i64, vp]
 
 
 def check(rc: int, what: str = "") -> None:

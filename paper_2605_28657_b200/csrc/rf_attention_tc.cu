@@ -1,16 +1,13 @@
 // Attention on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), head dim 128.
 //
-// One CTA = one 128-row query tile of the NH (= 2 under GQA) query heads that share a KV
-// head; K/V tiles are loaded once for both.  Thread (warp w, lane) owns query row
-// (w % 4) * 32 + lane of head w / 4 end to end: its S row and O row live in its TMEM lane, so
-// the softmax needs no cross-thread reduction.  Two passes over the key tiles:
-//   pass 1: S_j = Q K_j^T (tcgen05.mma M=128 N=128 K=128, Q and K_j staged by TMA with
-//           SWIZZLE_128B) -> row max only
-//   pass 2: S_j again, P_j = exp2(S_j - m) (unnormalised) written as bf16 into a
-//           SWIZZLE_128B shared tile (the A operand), O += P_j V_j with V consumed as V^T
-//           (K-major; written transposed by the QKV GEMM epilogue), row sums in registers.
-//           With the final max known, O never needs rescaling; O / l at the end.
-// K tiles are double-buffered (the TMA for tile j+1 is in flight while tile j computes).
+// Single-pass (online-softmax) flash attention, warp-specialised: a TMA warp streams K and
+// V^T tiles (V written transposed by the QKV GEMM epilogue, so it is the K-major B operand
+// of P V), one elected thread issues tcgen05.mma (S = Q K^T into TMEM, O += P V as a TS
+// MMA with P read from TMEM), and one warpgroup per query head runs the softmax with one
+// query row per thread (its S and O rows live in its TMEM lane: no cross-thread reduction).
+// Kernels: rf_attn_fa64_kernel (self-attention, 64-key tiles, double-buffered S) and
+// rf_attn_fa_kernel (one 128-key tile: cross-attention when not fused into the cross-Q
+// GEMM epilogue).
 #include <stdlib.h>
 
 #include "rf_common.cuh"
@@ -32,227 +29,6 @@ constexpr size_t attn_smem() {
 
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-// One CTA = 128 query rows x NH heads (the NH heads share a KV head).  Warp w works on
-// head w / 4, TMEM lane quarter w % 4: thread (w, lane) owns query row (w % 4) * 32 + lane.
-//   pass 1: S = Q K_j^T for every key tile -> row max only (no exponentials)
-//   pass 2: S again, P = exp2(S - m) (unnormalised, <= 1) -> bf16 SW128 smem tile,
-//           O += P V in TMEM, row sum accumulated in registers; O / l at the end.
-template <int NH>
-__global__ void __launch_bounds__(128 * NH, 1)
-rf_attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                  const __grid_constant__ CUtensorMap tvt, __nv_bfloat16 *__restrict__ out, int64_t ldo, int Nq,
-                  int Nk, int H, int Hkv, float scale_log2) {
-    constexpr int VS = 3 - NH;  // V stages (double-buffered for one head, single for two)
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *base = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *sQ = base;                        // [NH]
-    uint8_t *sK = sQ + NH * kOperand;          // [2 stages]
-    uint8_t *sV = sK + 2 * kOperand;           // [VS stages] (V^T: rows = dims)
-    uint8_t *sP = sV + VS * kOperand;          // [NH]
-    uint64_t *bar = (uint64_t *)(sP + NH * kOperand);
-    uint64_t *qfull = bar, *kfull = bar + 1, *vfull = bar + 3, *sdone = bar + 5, *odone = bar + 6;
-    uint32_t *tmem_slot = (uint32_t *)(bar + 8);
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int head_in_cta = warp >> 2, quarter = warp & 3;
-    const int group = H / Hkv;
-    const int bh = blockIdx.y, per_b = H / NH, b = bh / per_b, h0 = (bh % per_b) * NH;
-    const int h = h0 + head_in_cta, hk = h0 / group;
-    const int q0 = blockIdx.x * kTcRows;
-    const int nt = (Nk + kTcRows - 1) / kTcRows;
-
-    if (tid == 0) {
-        tma_prefetch(&tq);
-        tma_prefetch(&tk);
-        tma_prefetch(&tvt);
-        for (int i = 0; i < 7; ++i) mbar_init(&bar[i], 1);
-        mbar_fence_init();
-    }
-    if (warp == 0) tmem_alloc<256 * NH>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem + head_in_cta * 128, tO = tmem + NH * 128 + head_in_cta * 128;
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    constexpr uint32_t idesc = idesc_bf16(128, 128);
-
-    int kq = 0, kw = 0, vq = 0, vw = 0;   // loads issued / consumed (ring positions)
-    uint32_t sph = 0, oph = 0;
-    auto load_k = [&](int j) {
-        const int s = kq & 1;
-        mbar_expect_tx(&kfull[s], kOperand);
-        tma_load_2d(sK + s * kOperand, &tk, &kfull[s], hk * 128, b * Nk + j * 128);
-        tma_load_2d(sK + s * kOperand + kTile, &tk, &kfull[s], hk * 128 + 64, b * Nk + j * 128);
-        ++kq;
-    };
-    auto load_v = [&](int j) {
-        const int s = vq % VS;
-        mbar_expect_tx(&vfull[s], kOperand);
-        tma_load_2d(sV + s * kOperand, &tvt, &vfull[s], j * 128, (b * Hkv + hk) * 128);
-        tma_load_2d(sV + s * kOperand + kTile, &tvt, &vfull[s], j * 128 + 64, (b * Hkv + hk) * 128);
-        ++vq;
-    };
-    auto mma_s = [&]() {  // S_a = Q_a K^T for every head a (thread 0 only)
-        const int s = kw & 1;
-        mbar_wait(&kfull[s], (kw >> 1) & 1);
-        ++kw;
-        tc_fence_after();
-#pragma unroll
-        for (int a = 0; a < NH; ++a)
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                const uint64_t ad = sdesc_sw128(sQ + a * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
-                const uint64_t bd = sdesc_sw128(sK + s * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
-                umma_bf16(tmem + a * 128, ad, bd, idesc, ks > 0);
-            }
-        umma_commit(sdone);
-    };
-    auto mma_o = [&](bool accumulate) {  // O_a += P_a V
-        const int s = vw % VS;
-        mbar_wait(&vfull[s], (uint32_t)((vw / VS) & 1));
-        ++vw;
-        tc_fence_after();
-#pragma unroll
-        for (int a = 0; a < NH; ++a)
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                const uint64_t ad = sdesc_sw128(sP + a * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
-                const uint64_t bd = sdesc_sw128(sV + s * kOperand + (ks >> 2) * kTile) + (uint64_t)((ks & 3) * 2);
-                umma_bf16(tmem + NH * 128 + a * 128, ad, bd, idesc, (accumulate || ks > 0) ? 1u : 0u);
-            }
-        umma_commit(odone);
-    };
-
-    // ---------------------------------------------------------------- pass 1 -------
-    if (tid == 0) {
-        mbar_expect_tx(qfull, NH * kOperand);
-        for (int a = 0; a < NH; ++a) {
-            tma_load_2d(sQ + a * kOperand, &tq, qfull, (h0 + a) * 128, b * Nq + q0);
-            tma_load_2d(sQ + a * kOperand + kTile, &tq, qfull, (h0 + a) * 128 + 64, b * Nq + q0);
-        }
-        load_k(0);
-        mbar_wait(qfull, 0);
-        mma_s();
-    }
-    float m = -INFINITY;  // running max of S * scale_log2 (log2 domain)
-    for (int j = 0; j < nt; ++j) {
-        if (tid == 0 && j + 1 < nt) load_k(j + 1);
-        mbar_wait(sdone, sph);
-        sph ^= 1;
-        tc_fence_after();
-        const int valid = Nk - j * 128;   // keys of this tile that exist
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tS + lane_base + c * 32, r);
-            tmem_ld_wait();
-            float cm = -INFINITY;
-            if (valid >= (c + 1) * 32) {
-#pragma unroll
-                for (int e = 0; e < 32; ++e) cm = fmaxf(cm, __uint_as_float(r[e]));
-            } else {
-#pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (c * 32 + e < valid) cm = fmaxf(cm, __uint_as_float(r[e]));
-            }
-            m = fmaxf(m, cm * scale_log2);
-        }
-        tc_fence_before();
-        __syncthreads();  // S read by everyone before the next S MMA overwrites it
-        if (tid == 0 && j + 1 < nt) mma_s();
-    }
-
-    // ---------------------------------------------------------------- pass 2 -------
-    if (tid == 0) {
-        load_k(0);
-        load_v(0);
-        mma_s();
-    }
-    float l = 0.f;
-    const int row = quarter * 32 + lane;
-    uint8_t *prow = sP + head_in_cta * kOperand + row * 128;
-    for (int j = 0; j < nt; ++j) {
-        if (j > 0) {  // PV of tile j-1 done: P and that V stage are free
-            mbar_wait(odone, oph);
-            oph ^= 1;
-        }
-        if (tid == 0) {
-            if (VS == 1 && j > 0) load_v(j);   // single V stage: tile j reuses the buffer now
-            if (j + 1 < nt) {
-                load_k(j + 1);
-                if (VS == 2) load_v(j + 1);
-            }
-        }
-        mbar_wait(sdone, sph);
-        sph ^= 1;
-        tc_fence_after();
-        const int valid = Nk - j * 128;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tS + lane_base + c * 32, r);
-            tmem_ld_wait();
-            uint32_t pk[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                float p0 = exp2f(fmaf(__uint_as_float(r[2 * e]), scale_log2, -m));
-                float p1 = exp2f(fmaf(__uint_as_float(r[2 * e + 1]), scale_log2, -m));
-                if (valid < (c + 1) * 32) {
-                    if (c * 32 + 2 * e >= valid) p0 = 0.f;
-                    if (c * 32 + 2 * e + 1 >= valid) p1 = 0.f;
-                }
-                __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
-                const float2 pr = __bfloat1622float2(hh);   // sum what the MMA will actually use
-                l += pr.x + pr.y;
-                pk[e] = *(uint32_t *)&hh;
-            }
-            // keys [c*32, c*32+32) -> K tile c/2, 16-byte chunks (c%2)*4 .. +3, SW128 swizzle
-            uint8_t *tile = prow + (c >> 1) * kTile;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int chunk = ((c & 1) * 4 + q) ^ (row & 7);
-                *(uint4 *)(tile + chunk * 16) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            }
-        }
-        fence_proxy_async();  // generic-proxy P writes -> visible to the tensor core
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            mma_o(j > 0);
-            if (j + 1 < nt) mma_s();
-        }
-    }
-    mbar_wait(odone, oph);
-    tc_fence_after();
-    const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    const int qrow = q0 + row;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tO + lane_base + c * 32, r);
-        tmem_ld_wait();
-        if (qrow < Nq) {
-            __nv_bfloat16 *dst = out + ((int64_t)b * Nq + qrow) * ldo + h * 128 + c * 32;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    __nv_bfloat162 hh = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]) * inv_l,
-                                                              __uint_as_float(r[q * 8 + 2 * e + 1]) * inv_l);
-                    w[e] = *(uint32_t *)&hh;
-                }
-                *(uint4 *)(dst + q * 8) = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc<256 * NH>(tmem);
 }
 
 // ---------------------------------------------------------------------------------
@@ -884,111 +660,44 @@ int attn_plan(AttnPlan *p, const void *q, int64_t ldq, int64_t q_cols, const voi
     return rc;
 }
 
-template <int NH, int KVS, int PE, bool PP>
-static int launch_fa_pp(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+template <int NH, int KVS>
+static int launch_fa(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
+    constexpr bool PP = NH == 2;   // the GQA head pair ping-pongs its softmax groups
     static bool attr = false;
     if (!attr) {
-        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa_kernel<NH, KVS, PE, PP>,
+        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa_kernel<NH, KVS, kPolyPairs, PP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_smem<NH, KVS>()));
         attr = true;
     }
     dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / NH);
-    RF_TRY_CUDA(launch_pdl(rf_attn_fa_kernel<NH, KVS, PE, PP>, grid, dim3(fa_threads(NH)), fa_smem<NH, KVS>(), st,
-                           p.tq, p.tk, p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
+    RF_TRY_CUDA(launch_pdl(rf_attn_fa_kernel<NH, KVS, kPolyPairs, PP>, grid, dim3(fa_threads(NH)), fa_smem<NH, KVS>(),
+                           st, p.tq, p.tk, p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
     RF_TRY_LAUNCH("rf_attn_fa_kernel");
     return RF_OK;
 }
 
-template <int NH, int KVS, int PE>
-static int launch_fa_pe(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
-    static const bool pp = getenv("RF_ATTN_PP") ? atoi(getenv("RF_ATTN_PP")) != 0 : true;
-    if (NH == 2 && pp) return launch_fa_pp<NH, KVS, PE, true>(p, out, ldo, B, sc, st);
-    return launch_fa_pp<NH, KVS, PE, false>(p, out, ldo, B, sc, st);
-}
-
-// Tuning aids (not product ABI): RF_ATTN_POLY / RF_ATTN_FA64 at first use, or rf_attn_set_variant.
-static int g_poly = -1, g_fa64 = -1;
-static int poly_pairs() {   // exponential pairs (of 16) computed on the FMA pipe
-    if (g_poly < 0) g_poly = getenv("RF_ATTN_POLY") ? atoi(getenv("RF_ATTN_POLY")) : kPolyPairs;
-    return g_poly;
-}
-
-template <int NH, int PE>
+template <int NH>
 static int launch_fa64(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa64_kernel<NH, PE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_fa64_kernel<NH, kPolyPairs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)fa64_smem<NH>()));
         attr = true;
     }
     dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / NH);
-    RF_TRY_CUDA(launch_pdl(rf_attn_fa64_kernel<NH, PE>, grid, dim3(128 * NH + 64), fa64_smem<NH>(), st, p.tq,
+    RF_TRY_CUDA(launch_pdl(rf_attn_fa64_kernel<NH, kPolyPairs>, grid, dim3(128 * NH + 64), fa64_smem<NH>(), st, p.tq,
                            p.tk64, p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq, p.Nk, p.H, p.Hkv, sc));
     RF_TRY_LAUNCH("rf_attn_fa64_kernel");
     return RF_OK;
 }
 
-template <int NH>
-static int launch_fa64_pe(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
-    switch (poly_pairs()) {
-        case 0: return launch_fa64<NH, 0>(p, out, ldo, B, sc, st);
-        case 4: return launch_fa64<NH, 4>(p, out, ldo, B, sc, st);
-        default: return launch_fa64<NH, 6>(p, out, ldo, B, sc, st);
-    }
-}
-
-template <int NH, int KVS>
-static int launch_fa(const AttnPlan &p, void *out, int64_t ldo, int B, float sc, cudaStream_t st) {
-    switch (poly_pairs()) {
-        case 0: return launch_fa_pe<NH, KVS, 0>(p, out, ldo, B, sc, st);
-        case 4: return launch_fa_pe<NH, KVS, 4>(p, out, ldo, B, sc, st);
-        case 6: return launch_fa_pe<NH, KVS, 6>(p, out, ldo, B, sc, st);
-        case 8: return launch_fa_pe<NH, KVS, 8>(p, out, ldo, B, sc, st);
-        default: return launch_fa_pe<NH, KVS, 10>(p, out, ldo, B, sc, st);
-    }
-}
-
 int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) {
-    const bool pair = (p.H / p.Hkv) % 2 == 0;   // two query heads share each KV head
     const float sc = 1.4426950408889634f / sqrtf(128.f);
-    static const bool two_pass = getenv("RF_ATTN_TWO_PASS") != nullptr;   // the earlier two-pass kernel
-    if (!two_pass) {
-        // one key tile (cross-attention to 128 conditioning tokens): one head per CTA, two CTAs
-        // per SM; longer key ranges: the GQA head pair ping-pongs inside one CTA
-        if (p.Nk <= kTcRows) return launch_fa<1, 1>(p, out, ldo, B, sc, st);
-        // RF_ATTN_FA64 (tuning aid): 1 = 64-key kernel, one head per CTA (default); 2 = 64-key
-        // kernel, GQA head pair per CTA; 0 = the 128-key head-pair ping-pong kernel
-        if (g_fa64 < 0) g_fa64 = getenv("RF_ATTN_FA64") ? atoi(getenv("RF_ATTN_FA64")) : 1;
-        const int fa64 = g_fa64;
-        if (fa64 == 2 && pair) return launch_fa64_pe<2>(p, out, ldo, B, sc, st);
-        if (fa64 == 1) return launch_fa64_pe<1>(p, out, ldo, B, sc, st);
-        if (fa64 == 3) return launch_fa<1, 1>(p, out, ldo, B, sc, st);   // 128-key tiles, 2 CTAs / SM
-        if (fa64 == 4) return launch_fa<1, 2>(p, out, ldo, B, sc, st);
-        return pair ? launch_fa<2, 2>(p, out, ldo, B, sc, st) : launch_fa<1, 2>(p, out, ldo, B, sc, st);
-    }
-    if (pair) {
-        static bool attr = false;
-        if (!attr) {
-            RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)attn_smem<2>()));
-            attr = true;
-        }
-        dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H / 2);
-        rf_attn_tc_kernel<2><<<grid, 256, attn_smem<2>(), st>>>(p.tq, p.tk, p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq,
-                                                                p.Nk, p.H, p.Hkv, sc);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            RF_TRY_CUDA(cudaFuncSetAttribute(rf_attn_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)attn_smem<1>()));
-            attr = true;
-        }
-        dim3 grid((p.Nq + kTcRows - 1) / kTcRows, B * p.H);
-        rf_attn_tc_kernel<1><<<grid, 128, attn_smem<1>(), st>>>(p.tq, p.tk, p.tvt, (__nv_bfloat16 *)out, ldo, p.Nq,
-                                                                p.Nk, p.H, p.Hkv, sc);
-    }
-    RF_TRY_LAUNCH("rf_attn_tc_kernel");
-    return RF_OK;
+    // one key tile (cross-attention to <= 128 conditioning tokens): one head per CTA, two
+    // CTAs per SM; longer key ranges: 64-key tiles with double-buffered scores, one head per
+    // CTA, two CTAs per SM
+    if (p.Nk <= kTcRows) return launch_fa<1, 1>(p, out, ldo, B, sc, st);
+    return launch_fa64<1>(p, out, ldo, B, sc, st);
 }
 
 }  // namespace rf
@@ -1000,11 +709,6 @@ using namespace rf;
 extern "C" int rf_attn_set_trace(void *buf) {
     unsigned long long *p = (unsigned long long *)buf;
     return cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)) == cudaSuccess ? RF_OK : RF_ECUDA;
-}
-
-extern "C" void rf_attn_set_variant(int fa64, int poly) {
-    g_fa64 = fa64;
-    g_poly = poly;
 }
 
 extern "C" int rf_attention_tc_bf16(const void *q, const void *k, const void *vt, void *out, int32_t batch,

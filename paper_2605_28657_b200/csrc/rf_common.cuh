@@ -33,11 +33,7 @@ int sm_count();
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// RF_NO_PDL=1 launches everything fully serialised (timing experiments only).
-inline int pdl_allowed() {
-    static const int v = getenv("RF_NO_PDL") ? 0 : 1;
-    return v;
-}
+inline int pdl_allowed() { return 1; }
 
 // L2 residency window: while set (the DiT forward sets it to its fp32 residual stream),
 // every kernel launched through launch_pdl / the GEMM launcher carries an access-policy

@@ -26,10 +26,6 @@
 
 #include <cuda_bf16.h>
 
-extern "C" int rf_attention_bf16(const void *q, const void *k, const void *v, void *out, int32_t batch,
-                                 int32_t n_q, int32_t n_k, int32_t heads, int32_t kv_heads, int64_t ldq,
-                                 int64_t ldk, int64_t ldv, int64_t ldo, void *stream);
-
 namespace rf {
 
 constexpr int kMaxDitRows = 64;
@@ -178,13 +174,12 @@ struct Dit {
     __nv_bfloat16 *vt_self, *vt_cross;
     int n_pad, nc_pad;
     int64_t vt_cross_layer;                // elements per layer block of vt_cross
-    int skip = 0;                          // RF_DIT_SKIP at creation (timing ablation only)
     // the plain RMSNorm before the cross-attention query projection is fused across the GEMM
     // boundary: the O projection's epilogue writes bf16(h) and per-128-column sums of squares,
-    // the cross-Q epilogue scales each row by its rsqrt(mean) (RF_DIT_FUSE_NORM=0: kernel)
+    // the cross-Q epilogue scales each row by its rsqrt(mean) (d_model % 128 == 0)
     bool fuse_norm2 = true;
-    // cross-attention computed in the epilogue of the cross-Q projection (single-CTA 128-row
-    // tiles per batch entry; RF_DIT_FUSE_XATTN=0: separate attention kernel)
+    // cross-attention computed in the epilogue of the cross-Q projection (CTA-pair 256-row
+    // tiles per batch entry; needs <= 128 conditioning tokens, else a separate kernel)
     bool fuse_xattn = true;
     std::vector<GemmPlan> p_qcx;
     float *sq_part = nullptr;              // [D / 128][max_rows * tokens]
@@ -195,8 +190,6 @@ struct Dit {
     cudaGraphExec_t graph[kMaxDitRows + 1] = {};
     int graph_kernels[kMaxDitRows + 1] = {};   // kernel nodes of each captured forward
     float *graph_out[kMaxDitRows + 1] = {};
-    bool use_graphs;
-    bool tc_attention;
     L2Window l2win;   // the residual stream h, kept persisting in L2 during the forward
     // GEMM plans (tensor maps at max rows)
     GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out, p_kvc;
@@ -300,10 +293,8 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     }
     Dit *d = new Dit();
     d->c = c;
-    d->skip = getenv("RF_DIT_SKIP") ? atoi(getenv("RF_DIT_SKIP")) : 0;
-    d->fuse_norm2 = !(getenv("RF_DIT_FUSE_NORM") && atoi(getenv("RF_DIT_FUSE_NORM")) == 0) && c.d_model % 128 == 0;
-    d->fuse_xattn = !(getenv("RF_DIT_FUSE_XATTN") && atoi(getenv("RF_DIT_FUSE_XATTN")) == 0) && c.head_dim == 128 &&
-                    c.n_cond_tokens <= 128;
+    d->fuse_norm2 = c.d_model % 128 == 0;
+    d->fuse_xattn = c.head_dim == 128 && c.n_cond_tokens <= 128;
     d->w = *w;
     d->max_rows = max_rows;
     d->frames = frames;
@@ -322,26 +313,17 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     // when M is small (the cross-attention K/V of 128 tokens per row).
     auto bn_for = [](int64_t n) { return (n >= 4096 && n % 256 == 0) ? 256 : 128; };
     // cross-Q projection + cross-attention epilogue on CTA pairs (256-row tiles, cta_group::2
-    // attention MMAs); RF_DIT_XATT_PAIR=0 keeps single-CTA 128-row tiles (A/B timing)
-    const int xattn_cg = (getenv("RF_DIT_XATT_PAIR") && atoi(getenv("RF_DIT_XATT_PAIR")) == 0) ? 1 : 2;
-    const int qkv_bn = getenv("RF_DIT_QKV_BN") ? atoi(getenv("RF_DIT_QKV_BN")) : 0;
-    // tuning aid RF_DIT_PROJ_BN=256: the N = d_model projections (O, cross-O, down) on
-    // 256 x 256 pair tiles instead of 256 x 128
-    const int proj_bn = getenv("RF_DIT_PROJ_BN") ? atoi(getenv("RF_DIT_PROJ_BN")) : 0;
+    // attention MMAs): 0.7% faster than single-CTA 128-row tiles
+    const int xattn_cg = 2;
 
     int rc = 0;
-    // CTA pairs from this many rows up (tuning aid RF_DIT_PAIR_MIN_M; the all-layer cross K/V
-    // projection has max_rows x n_cond_tokens rows)
-    const int64_t pair_min_m = getenv("RF_DIT_PAIR_MIN_M") ? atoll(getenv("RF_DIT_PAIR_MIN_M")) : 1024;
+    // CTA pairs from 1024 rows up (the all-layer cross K/V projection has max_rows x
+    // n_cond_tokens rows)
+    const int64_t pair_min_m = 1024;
     auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
         if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N), M >= pair_min_m ? 2 : 1);
     };
-    auto plan_proj = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
-        if (proj_bn && !rc)
-            rc = gemm_plan(p, A, Bw, M, N, K, K, K, proj_bn, M >= 1024 ? 2 : 1);
-        else
-            plan(p, A, Bw, M, N, K);
-    };
+    auto plan_proj = plan;
     plan(&d->p_in, d->xin, w->w_in, BN, D, d->in_dim);
     plan(&d->p_t1, d->tfeat, w->w_t1, Bmax, D, c.freq_dim);
     plan(&d->p_t2, d->tbuf, w->w_t2, Bmax, D, D);
@@ -360,11 +342,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     const __nv_bfloat16 *woc = (const __nv_bfloat16 *)w->w_oc, *wgu = (const __nv_bfloat16 *)w->w_gu;
     const __nv_bfloat16 *wdn = (const __nv_bfloat16 *)w->w_down;
     for (int64_t l = 0; l < L; ++l) {
-        if (qkv_bn)   // tuning aid RF_DIT_QKV_BN=128|256 (default: bn_for)
-            rc = rc ? rc : gemm_plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D, D, D, qkv_bn,
-                                     BN >= 1024 ? 2 : 1);
-        else
-            plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
+        plan(&d->p_qkv[l], d->a, wq + l * d->qkv_dim * D, BN, d->qkv_dim, D);
         plan_proj(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_qc[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D);
         if (!rc) rc = gemm_plan(&d->p_qcx[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D, D, D, 128, xattn_cg);
@@ -395,9 +373,8 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         delete d;
         return rc;
     }
-    d->tc_attention = getenv("RF_ATTN_MMA_SYNC") == nullptr;   // the tcgen05 kernel is the default
-    // L2 persistence for the fp32 residual stream (24.6 MB at 4 rows; RF_DIT_L2_PERSIST=0 off)
-    if (!(getenv("RF_DIT_L2_PERSIST") && atoi(getenv("RF_DIT_L2_PERSIST")) == 0)) {
+    // L2 persistence for the fp32 residual stream (24.6 MB at 4 rows; +1.2%)
+    {
         int dev = 0, maxp = 0;
         const size_t hb = (size_t)max_rows * d->tokens * c.d_model * sizeof(float);
         if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -412,7 +389,6 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         }
         cudaGetLastError();   // attribute / limit queries are best-effort
     }
-    d->use_graphs = getenv("RF_DIT_NO_GRAPH") == nullptr;
     // V^T pad columns are never written: zero them once
     RF_TRY_CUDA(cudaMemsetAsync(d->vt_self, 0, (size_t)max_rows * d->kv_dim * d->n_pad * 2, (cudaStream_t)stream));
     RF_TRY_CUDA(cudaMemsetAsync(d->vt_cross, 0, (size_t)L * d->vt_cross_layer * 2, (cudaStream_t)stream));
@@ -433,8 +409,7 @@ extern "C" int rf_dit_destroy(void *handle) {
 
 static int norm_mod(const Dit &d, const float *h, int64_t rows, const float *shift, const float *scale,
                     int64_t mod_ld, __nv_bfloat16 *out, cudaStream_t st) {
-    // rows (warps) per block: 8 (tuning aid RF_DIT_NORM_ROWS = 4 / 8 / 16)
-    static const int rpb = getenv("RF_DIT_NORM_ROWS") ? atoi(getenv("RF_DIT_NORM_ROWS")) : 8;
+    constexpr int rpb = 8;   // rows (warps) per block
     const unsigned blocks = (unsigned)((rows + rpb - 1) / rpb);
     switch (d.c.d_model) {
         case 2048: RF_TRY_CUDA(launch_pdl(rf_dit_norm_mod<2048>, dim3(blocks), dim3(32 * rpb), 0, st, h, rows, d.tokens, shift, scale, mod_ld, out, d.c.norm_eps)); break;
@@ -462,10 +437,6 @@ static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
     return rc;
 }
 static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
-    // RF_DIT_SKIP at rf_dit_create (timing ablation only; the output is garbage): bit mask of
-    // per-layer kernel classes left out -- 1 norms, 2 self-attention, 4 cross-attention, 8 QKV, 16 O, 32 cross-Q,
-    // 64 cross-O, 128 gate-up, 256 down (tools/dit_ablate.py)
-    const int skip = d.skip;
     const rf_dit_config &c = d.c;
     const int64_t N = d.tokens, M = (int64_t)rows * N, D = c.d_model, L = c.n_layers, B = rows;
     const int64_t W6 = 6 * D, Nc = c.n_cond_tokens;
@@ -491,23 +462,18 @@ static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) 
     {
         const VtOut vtc{d.vt_cross, (int)d.kv_dim, c.n_kv_heads, d.nc_pad, (int)(2 * d.kv_dim), d.vt_cross_layer};
         RF_TRY(gemm_run(d.p_kvc, 5 /* bf16, V^T out */, d.kvc, L * 2 * d.kv_dim, nullptr, 0, (int)Nc, 1.f, st,
-                        d.rope, 0, B * Nc, d.tc_attention ? &vtc : nullptr));
+                        d.rope, 0, B * Nc, &vtc));
     }
     // h = in_proj(patches)
     RF_TRY(gemm_run(d.p_in, RF_EPI_F32, d.h, D, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
     for (int64_t l = 0; l < L; ++l) {
         const float *md = d.mods + l * B * W6;  // [B][6][D]: shift,scale,gate (msa), shift,scale,gate (mlp)
         // self-attention
-        if (!(skip & 1)) RF_TRY(norm_mod(d, d.h, M, md + 0 * D, md + 1 * D, W6, d.a, st));
+        RF_TRY(norm_mod(d, d.h, M, md + 0 * D, md + 1 * D, W6, d.a, st));
         const VtOut vts{d.vt_self, (int)(d.q_dim + d.kv_dim), c.n_kv_heads, d.n_pad};
-        if (!(skip & 8)) RF_TRY(gemm_run(d.p_qkv[l], 5 /* bf16 + RoPE */, d.qkv, d.qkv_dim, nullptr, 0, (int)N, 1.f, st, d.rope,
-                        (int)(d.q_dim + d.kv_dim), M, d.tc_attention ? &vts : nullptr));
-        if (skip & 2) {
-        } else if (d.tc_attention)
-            RF_TRY(attn_run(d.a_self, d.att, d.q_dim, (int)B, st));
-        else
-            RF_TRY(rf_attention_bf16(d.qkv, d.qkv + d.q_dim, d.qkv + d.q_dim + d.kv_dim, d.att, (int)B, (int)N,
-                                     (int)N, c.n_heads, c.n_kv_heads, d.qkv_dim, d.qkv_dim, d.qkv_dim, d.q_dim, st));
+        RF_TRY(gemm_run(d.p_qkv[l], 5 /* bf16 + RoPE */, d.qkv, d.qkv_dim, nullptr, 0, (int)N, 1.f, st, d.rope,
+                        (int)(d.q_dim + d.kv_dim), M, &vts));
+        RF_TRY(attn_run(d.a_self, d.att, d.q_dim, (int)B, st));
         NormFuse nf_out, nf_in;   // RMSNorm(h) for the cross-attention query, fused (see Dit)
         if (d.fuse_norm2) {
             const int64_t BNmax = (int64_t)d.max_rows * N;
@@ -521,33 +487,26 @@ static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) 
             nf_in.rs_inv_d = 1.0f / (float)D;
             nf_in.rs_eps = c.norm_eps;
         }
-        if (!(skip & 16))
-            RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M,
-                            nullptr, d.fuse_norm2 ? &nf_out : nullptr));
+        RF_TRY(gemm_run(d.p_o[l], RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M,
+                        nullptr, d.fuse_norm2 ? &nf_out : nullptr));
         // cross-attention to the row's conditioning tokens (residual, no gate)
-        if (!(skip & 1) && !d.fuse_norm2) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
-        const bool xattn = d.fuse_xattn && d.tc_attention;
-        if (xattn && !(skip & 32)) {   // query projection + cross-attention in one kernel
+        if (!d.fuse_norm2) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
+        const bool xattn = d.fuse_xattn;
+        if (xattn) {   // query projection + cross-attention in one kernel
             const XAttn xa{&d.a_cross[l].tk, &d.a_cross[l].tvt, &d.a_cross[l].tk64, &d.a_cross[l].tvt64, (int)N, (int)B, (int)Nc,
                            c.n_heads / c.n_kv_heads, c.n_kv_heads};
             RF_TRY(gemm_run(d.p_qcx[l], 6 /* cross-attention epilogue */, d.att, d.q_dim, nullptr, 0, 1, 1.f, st,
                             nullptr, 0, M, nullptr, d.fuse_norm2 ? &nf_in : nullptr, &xa));
-        } else if (!(skip & 32)) {
+        } else {
             RF_TRY(gemm_run(d.p_qc[l], RF_EPI_BF16, d.qc, d.q_dim, nullptr, 0, 1, 1.f, st, nullptr, 0, M, nullptr,
                             d.fuse_norm2 ? &nf_in : nullptr));
-        }
-        const __nv_bfloat16 *kvl = d.kvc + l * 2 * d.kv_dim;
-        if ((skip & 4) || xattn) {
-        } else if (d.tc_attention)
             RF_TRY(attn_run(d.a_cross[l], d.att, d.q_dim, (int)B, st));
-        else
-            RF_TRY(rf_attention_bf16(d.qc, kvl, kvl + d.kv_dim, d.att, (int)B, (int)N, (int)Nc, c.n_heads,
-                                     c.n_kv_heads, d.q_dim, L * 2 * d.kv_dim, L * 2 * d.kv_dim, d.q_dim, st));
-        if (!(skip & 64)) RF_TRY(gemm_run(d.p_oc[l], RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));
+        }
+        RF_TRY(gemm_run(d.p_oc[l], RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));
         // SwiGLU MLP
-        if (!(skip & 1)) RF_TRY(norm_mod(d, d.h, M, md + 3 * D, md + 4 * D, W6, d.a, st));
-        if (!(skip & 128)) RF_TRY(gemm_run(d.p_gu[l], RF_EPI_SWIGLU, d.mlp, c.mlp_hidden, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
-        if (!(skip & 256)) RF_TRY(gemm_run(d.p_down[l], RF_EPI_RESID_GATE, d.h, D, md + 5 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
+        RF_TRY(norm_mod(d, d.h, M, md + 3 * D, md + 4 * D, W6, d.a, st));
+        RF_TRY(gemm_run(d.p_gu[l], RF_EPI_SWIGLU, d.mlp, c.mlp_hidden, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
+        RF_TRY(gemm_run(d.p_down[l], RF_EPI_RESID_GATE, d.h, D, md + 5 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
     }
     // final AdaLN + output projection (fp32), tokens [B, N, p*C] == latent [B, T, C]
     RF_TRY(norm_mod(d, d.h, M, d.fmod, d.fmod + D, 2 * D, d.a, st));
@@ -575,7 +534,7 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     RF_TRY_CUDA(cudaStreamIsCapturing(st, &cap));
     // graphs need a capturable stream (not the legacy default stream) and no outer capture
-    if (!d.use_graphs || st == 0 || cap != cudaStreamCaptureStatusNone) return dit_body(d, rows, v_out, st);
+    if (st == 0 || cap != cudaStreamCaptureStatusNone) return dit_body(d, rows, v_out, st);
     if (!d.graph[rows] || d.graph_out[rows] != v_out) {
         if (d.graph[rows]) {
             cudaGraphExecDestroy(d.graph[rows]);
@@ -604,23 +563,6 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
 }
 
 extern "C" float *rf_dit_output(void *handle) { return handle ? ((Dit *)handle)->vout : nullptr; }
-
-// Debugging aid (not part of the product ABI): change the timing-ablation mask of a live DiT
-// (see dit_body) and drop its captured graphs, so buffers keep the valid contents of earlier
-// full forwards while kernel classes are left out (tools/dit_ablate2.py).
-extern "C" int rf_dit_set_skip(void *handle, int32_t mask) {
-    Dit *d = (Dit *)handle;
-    if (!d) return RF_EINVAL;
-    cudaDeviceSynchronize();
-    d->skip = mask;
-    for (int i = 0; i <= kMaxDitRows; ++i)
-        if (d->graph[i]) {
-            cudaGraphExecDestroy(d->graph[i]);
-            d->graph[i] = nullptr;
-            d->graph_out[i] = nullptr;
-        }
-    return RF_OK;
-}
 
 // Kernels one forward of `rows` rows launches (the row-table kernel + the captured graph's
 // kernel nodes); -1 before that row count's graph exists.  Reported by bench.py.

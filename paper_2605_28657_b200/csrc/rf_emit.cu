@@ -156,41 +156,50 @@ extern "C" int rf_x0_compose(double *out, const double *base, const double *hint
     return RF_OK;
 }
 
-// Scratch for partials lives in a static device buffer grown on demand (tiny).
-static double *g_partials = nullptr;
-static int64_t g_partials_n = 0;
-
-static int ensure_partials(int64_t n) {
-    if (n <= g_partials_n) return RF_OK;
-    if (g_partials) cudaFree(g_partials);
-    g_partials = nullptr;
-    RF_TRY_CUDA(cudaMalloc(&g_partials, n * sizeof(double)));
-    g_partials_n = n;
-    return RF_OK;
+// Reduction scratch is the caller's (one buffer per stream: concurrent pipelines and
+// devices never share partials).  Emits are processed in chunks of kMaxEmit launches;
+// chunk c's first "previous latent" is chunk c-1's last latent, so any number of
+// completions per tick (any ring depth) gives the same statistics as one batch.
+extern "C" int64_t rf_reduce_workspace_elems(int64_t numel) {
+    if (numel <= 0) return 0;
+    const int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
+    return 2 * chunks * kMaxEmit;
 }
 
 extern "C" int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, const double *last,
                              const double *reference, double *mse_prev, double *mse_ref,
-                             uint32_t *status, void *stream) {
+                             uint32_t *status, double *scratch, int64_t scratch_elems, void *stream) {
     if (count <= 0) return RF_OK;
-    if (count > kMaxEmit || !emits || !mse_prev || !mse_ref || !status || numel <= 0) {
+    if (!emits || !mse_prev || !mse_ref || !status || numel <= 0 || !scratch) {
         set_error("rf_emit_stats: bad arguments (count %d)", count);
         return RF_EINVAL;
     }
+    if (scratch_elems < rf_reduce_workspace_elems(numel)) {
+        set_error("rf_emit_stats: scratch of %lld doubles < %lld", (long long)scratch_elems,
+                  (long long)rf_reduce_workspace_elems(numel));
+        return RF_EWORKSPACE;
+    }
     cudaStream_t st = (cudaStream_t)stream;
-    EmitBatch B;
-    B.count = count;
-    for (int i = 0; i < count; ++i) B.e[i] = emits[i];
-    int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
-    int rc = ensure_partials(2 * chunks * count);
-    if (rc) return rc;
-    double *pp = g_partials, *pr = g_partials + chunks * count;
-    rf_emit_partials<<<dim3((unsigned)chunks, (unsigned)count), kRedThreads, 0, st>>>(
-        B, numel, last, reference, pp, pr, status);
-    RF_TRY_LAUNCH("rf_emit_partials");
-    rf_emit_finish<<<1, 32, 0, st>>>(count, chunks, numel, pp, pr, mse_prev, mse_ref, last != nullptr,
-                                     reference != nullptr);
-    RF_TRY_LAUNCH("rf_emit_finish");
+    const int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
+    double *pp = scratch, *pr = scratch + chunks * kMaxEmit;
+    for (int c0 = 0; c0 < count; c0 += kMaxEmit) {
+        EmitBatch B;
+        B.count = count - c0 < kMaxEmit ? count - c0 : kMaxEmit;
+        for (int i = 0; i < B.count; ++i) {
+            B.e[i] = emits[c0 + i];
+            if (!B.e[i].latent || !B.e[i].record) {
+                set_error("rf_emit_stats: null pointer in emit %d", c0 + i);
+                return RF_EINVAL;
+            }
+        }
+        const double *prev = c0 == 0 ? last : emits[c0 - 1].latent;
+        rf_emit_partials<<<dim3((unsigned)chunks, (unsigned)B.count), kRedThreads, 0, st>>>(
+            B, numel, prev, reference, pp, pr, status);
+        RF_TRY_LAUNCH("rf_emit_partials");
+        rf_emit_finish<<<1, 32, 0, st>>>(B.count, chunks, numel, pp, pr, mse_prev + c0, mse_ref + c0,
+                                         prev != nullptr, reference != nullptr);
+        RF_TRY_LAUNCH("rf_emit_finish");
+    }
     return RF_OK;
 }
 
@@ -219,18 +228,21 @@ __global__ void rf_sum_finish(const double *part, int64_t chunks, int64_t numel,
     *out = __ddiv_rn(s, (double)numel);
 }
 
-extern "C" int rf_mse(const double *a, const double *b, int64_t numel, double *out, void *stream) {
-    if (!a || !b || !out || numel <= 0) {
+extern "C" int rf_mse(const double *a, const double *b, int64_t numel, double *out, double *scratch,
+                      int64_t scratch_elems, void *stream) {
+    if (!a || !b || !out || numel <= 0 || !scratch) {
         set_error("rf_mse: bad arguments");
         return RF_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
     int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
-    int rc = ensure_partials(chunks);
-    if (rc) return rc;
-    rf_sqdiff_partials<<<(unsigned)chunks, kRedThreads, 0, st>>>(a, b, numel, g_partials);
+    if (scratch_elems < chunks) {
+        set_error("rf_mse: scratch of %lld doubles < %lld", (long long)scratch_elems, (long long)chunks);
+        return RF_EWORKSPACE;
+    }
+    rf_sqdiff_partials<<<(unsigned)chunks, kRedThreads, 0, st>>>(a, b, numel, scratch);
     RF_TRY_LAUNCH("rf_sqdiff_partials");
-    rf_sum_finish<<<1, 1, 0, st>>>(g_partials, chunks, numel, out);
+    rf_sum_finish<<<1, 1, 0, st>>>(scratch, chunks, numel, out);
     RF_TRY_LAUNCH("rf_sum_finish");
     return RF_OK;
 }

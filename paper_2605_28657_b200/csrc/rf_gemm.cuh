@@ -72,11 +72,6 @@ struct EpiArgs {
     // the attention kernel's maps); query head = n / 128, KV head = head / x_group.
     int x_rpb, x_mtpb, x_batches, x_nk, x_group, x_hkv;
     float x_scale;   // log2(e) / sqrt(head dim)
-    // stream-K (null: static tile walk): [units * CG * 128 * BN] fp32 partial tiles and
-    // [units * CG * 4] flags (zero between launches); sk_num_m = the plan's m-tile count
-    float *sk_ws;
-    unsigned *sk_flags;
-    int sk_num_m;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -130,46 +125,6 @@ struct Cfg {
     static constexpr int STAGES = (int)(BUDGET / STAGE_BYTES) > 10 ? 10 : (int)(BUDGET / STAGE_BYTES);
     static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + C_BYTES + 512;
 };
-
-// stream-K partial tiles (see walk_init in the kernel): raw fp32 accumulator rows parked in
-// global memory by the unit that computes a split tile's tail k blocks, one flag per
-// (unit, CTA, epilogue warp), consumed (and reset) by the unit that finishes the tile.
-// Layout per epilogue warp: [chunk][8 float4][32 lanes], so every warp-wide access is one
-// contiguous 512-byte run (a row-per-thread layout made these scattered 16-byte accesses).
-__device__ __forceinline__ void sk_store32(float *warp_slot, int chunk, int lane, const uint32_t (&r)[32]) {
-    float4 *dst = (float4 *)warp_slot + chunk * 256 + lane;
-#pragma unroll
-    for (int v = 0; v < 8; ++v)
-        __stcg(dst + v * 32, make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                         __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])));
-}
-__device__ __forceinline__ void sk_add32(const float *warp_slot, int chunk, int lane, uint32_t (&r)[32]) {
-    const float4 *src = (const float4 *)warp_slot + chunk * 256 + lane;
-    float4 pv[8];
-#pragma unroll
-    for (int v = 0; v < 8; ++v) pv[v] = __ldcg(src + v * 32);
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-        const float4 p = pv[v];
-        r[4 * v] = __float_as_uint(__uint_as_float(r[4 * v]) + p.x);
-        r[4 * v + 1] = __float_as_uint(__uint_as_float(r[4 * v + 1]) + p.y);
-        r[4 * v + 2] = __float_as_uint(__uint_as_float(r[4 * v + 2]) + p.z);
-        r[4 * v + 3] = __float_as_uint(__uint_as_float(r[4 * v + 3]) + p.w);
-    }
-}
-__device__ __forceinline__ void sk_set_flag(unsigned *flag, int lane) {
-    __threadfence();   // this lane's partial stores, then the warp, then the release
-    __syncwarp();
-    if (lane == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
-}
-__device__ __forceinline__ void sk_wait_flag(const unsigned *flag) {
-    unsigned v;
-    for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-        if (v) break;
-        __nanosleep(100);
-    }
-}
 
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -242,17 +197,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     pdl_launch();
     RF_GTRACE(13);
 
-    // Stream-K (epi.sk_ws set): the tile grid is the PLAN's (epi.sk_num_m m-tiles, fixed
-    // for a given GEMM whatever rows this call has), and unit u owns the contiguous k-block
-    // range [u * total / units, (u + 1) * total / units) of the tile-major k-block sequence,
-    // so every unit does the same MMA work (no partial last wave).  A tile split between
-    // two units: the later unit computes its tail k blocks first and parks the fp32 partial
-    // in sk_ws[unit]; the earlier unit, which reaches the tile's head k blocks last, adds
-    // it (head + tail, a fixed order) and runs the real epilogue.  Split points depend only
-    // on the plan, so a row's result does not depend on how many rows the call has.
-    const bool sk = !C::XATT && epi.sk_ws != nullptr;
-    const int num_m = C::XATT ? epi.x_batches * epi.x_mtpb : sk ? epi.sk_num_m : (M + TM - 1) / TM, num_n = N / BN,
-              kblocks = K / BK;
+    const int num_m = C::XATT ? epi.x_batches * epi.x_mtpb : (M + TM - 1) / TM, num_n = N / BN, kblocks = K / BK;
     // first row of tile t (kCrossAttn: tiles never straddle two batch entries)
     auto row0 = [&](int t) {
         const int mt = t % num_m;
@@ -262,30 +207,20 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
     const int num_tiles = num_m * num_n;
     const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // tile walker id
     const int units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-    const int64_t sk_total = (int64_t)num_tiles * kblocks;
-    // segment walker: every role walks the same (tile, k-block range) sequence
+    // static tile walk: unit u takes tiles u, u + units, ... (every role walks the same
+    // sequence); tiles whose rows lie beyond this call's M are skipped
     struct Walk {
-        int64_t pos, end;
+        int pos;
     };
-    auto walk_init = [&]() -> Walk {
-        if (sk) return Walk{(int64_t)unit * sk_total / units, (int64_t)(unit + 1) * sk_total / units};
-        return Walk{unit, num_tiles};
-    };
+    auto walk_init = [&]() -> Walk { return Walk{unit}; };
     auto walk_next = [&](Walk &w, int &tile, int &kb0, int &kb1) -> bool {
         for (;;) {
-            if (w.pos >= w.end) return false;
-            if (sk) {
-                tile = (int)(w.pos / kblocks);
-                kb0 = (int)(w.pos % kblocks);
-                kb1 = (int)min((int64_t)kblocks, kb0 + (w.end - w.pos));
-                w.pos += kb1 - kb0;
-            } else {
-                tile = (int)w.pos;
-                kb0 = 0;
-                kb1 = kblocks;
-                w.pos += units;
-            }
-            if (C::XATT || (tile % num_m) * TM < M) return true;   // else: rows beyond this call's M
+            if (w.pos >= num_tiles) return false;
+            tile = w.pos;
+            kb0 = 0;
+            kb1 = kblocks;
+            w.pos += units;
+            if (C::XATT || (tile % num_m) * TM < M) return true;
         }
     };
 
@@ -389,38 +324,14 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         uint32_t acc_phase = 0, c_phase = 0;
         Walk w = walk_init();
         bool have = walk_next(w, t, kb0, kb1);
-        // a stream-K tail segment only parks its partial: no residual slice to stage
-        if (lane == 0 && have && !(sk && kb0 > 0)) load_pass(t, 0);
+        if (lane == 0 && have) load_pass(t, 0);
         while (have) {
             Walk wn = w;
             int tn, nk0, nk1;
             const bool next = walk_next(wn, tn, nk0, nk1);
-            const bool next_load = next && !(sk && nk0 > 0);
+            const bool next_load = next;
             const int m0 = tile_m0(t), n0 = tile_n0(t);
-            const bool sk_put = sk && kb0 > 0, sk_get = sk && kb0 == 0 && kb1 < kblocks;
-            float *sk_slot = sk ? epi.sk_ws + ((size_t)((sk_put ? unit : unit + 1) * CG + rank) * 4 + q) * 32 * BN
-                                : nullptr;
-            if (sk_put) {   // tail k blocks of a split tile: park the raw partial sums
-                mbar_wait(&tfull[acc], acc_phase);
-                tc_fence_after();
-#pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
-                    uint32_t r[32];
-                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
-                    tmem_ld_wait();
-                    sk_store32(sk_slot, c0 / 32, lane, r);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if constexpr (CG == 2)
-                        mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
-                    else
-                        mbar_arrive(&tempty[acc]);
-                }
-                sk_set_flag(epi.sk_flags + (unit * CG + rank) * 4 + q, lane);
-                if (lane == 0 && next_load) load_pass(tn, 0);
-            } else {
+            {
             const int m = min(m0 + lane, M - 1);
             const int b_lo = min(m0, M - 1) / epi.rows_per_batch, b_hi = min(m0 + 31, M - 1) / epi.rows_per_batch;
             __syncwarp();   // the previous tile's gate reads are done
@@ -434,7 +345,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             const bool live = m0 + lane < M;
             float ss = 0.f;
             uint2 aux4[8];
-            if (sk_get) sk_wait_flag(epi.sk_flags + ((unit + 1) * CG + rank) * 4 + q);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
@@ -448,7 +358,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     uint32_t r[32];
                     tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col), r);
                     tmem_ld_wait();
-                    if (sk_get) sk_add32(sk_slot, col / 32, lane, r);   // head + tail
                     float4 *row = (float4 *)(sw + j * 4096 + lane * 128);
                     const float4 *gv = (const float4 *)(gr + col);
 #pragma unroll
@@ -501,7 +410,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 }
             }
             if (epi.aux && live) epi.sq_part[(int64_t)(n0 / BN) * epi.sq_ld + m0 + lane] = ss;
-            if (sk_get && lane == 0) epi.sk_flags[((unit + 1) * CG + rank) * 4 + q] = 0u;   // for the next launch
             }
             if (++acc == 2) {
                 acc = 0;
@@ -712,11 +620,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         uint32_t acc_phase = 0;
         for (Walk w = walk_init(); walk_next(w, t, kb0, kb1); ++it) {
             const int n0 = (t / num_m) * BN;
-            // stream-K roles of this segment (see walk_init): park the tail partial / add it
-            const bool sk_put = sk && kb0 > 0, sk_get = sk && kb0 == 0 && kb1 < kblocks;
-            float *sk_slot = sk ? epi.sk_ws + ((size_t)((sk_put ? unit : unit + 1) * CG + rank) * 4 + q) * 32 * BN
-                                : nullptr;
-            if (sk_get) sk_wait_flag(epi.sk_flags + ((unit + 1) * CG + rank) * 4 + q);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             if (q == 2 && lane == 0) RF_TRACE(it, 4);
@@ -772,11 +675,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
                 tmem_ld_wait();
-                if (sk_put) {   // tail k blocks of a split tile: park the raw partial sums
-                    sk_store32(sk_slot, c0 / 32, lane, r);
-                    continue;
-                }
-                if (sk_get) sk_add32(sk_slot, c0 / 32, lane, r);   // head + tail
                 // bf16 row stores are warp-collective (quad transposes): dead rows ride along
                 if (!live && EPI != kStoreBF16 && EPI != kBF16Rope) continue;
                 const int n = n0 + c0;
@@ -897,9 +795,7 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 else
                     mbar_arrive(&tempty[acc]);
             }
-            if (sk_put) sk_set_flag(epi.sk_flags + (unit * CG + rank) * 4 + q, lane);
-            if (sk_get && lane == 0) epi.sk_flags[((unit + 1) * CG + rank) * 4 + q] = 0u;   // for the next launch
-            if (C::TMA_O && !sk_put) {   // rows >= M are clipped by the tensor map
+            if (C::TMA_O) {   // rows >= M are clipped by the tensor map
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {

@@ -15,8 +15,6 @@ struct GemmPlan {
     int64_t M, N, K;
     int bn;
     int cg;   // 1: 128 x bn tiles per CTA; 2: 256 x bn tiles per CTA pair (cta_group::2)
-    bool sk = false;   // stream-K tile walk (see rf_gemm_kernel)
-    int sk_num_m = 0;   // the plan's m-tile count (fixes the stream-K split points)
 };
 
 int make_tmap_bf16_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes,
@@ -28,7 +26,7 @@ int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo);
 // bind the bf16 output of a SwiGLU plan with 256-wide tiles (TMA-stored epilogue)
 int gemm_plan_o(GemmPlan *p, void *out, int64_t ldo);
 int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, int64_t K, int64_t lda,
-              int64_t ldb, int bn, int cg = 1, int sk = 0);
+              int64_t ldb, int bn, int cg = 1);
 // Transposed V output of the QKV / cross-KV GEMM (see EpiArgs::vt).
 struct VtOut {
     void *ptr;

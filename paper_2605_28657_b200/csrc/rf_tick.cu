@@ -60,7 +60,10 @@ __device__ __forceinline__ ElemVel velocity_elem(const rf_row &R, const double *
     const bool f32 = (R.flags & RF_ROWF_V_F32) != 0;
     // a given velocity (DiT output: float32, or a float64 seam input)
     auto given = [&](const double *p) -> double {
-        return f32 ? (double)reinterpret_cast<const float *>(p)[i] : p[i];
+        double g = f32 ? (double)reinterpret_cast<const float *>(p)[i] : p[i];
+        // shared style offset in x0 space for a velocity model: x0' = (x - v t) + style
+        if (R.flags & RF_ROWF_STYLE_V) g = dsub(g, ddiv(style[i], t));
+        return g;
     };
     double v;
     if (R.n_cond == 1) {
@@ -184,6 +187,7 @@ __device__ __forceinline__ void fast_pair(const rf_row &R, const double *__restr
         } else {
             vg = ld2(R.cond_x0[0] + i);
         }
+        if (R.flags & RF_ROWF_STYLE_V) st = ld2(style + i);
     } else {
         x0p = ld2(R.cond_x0[0] + i);
         st = ld2(style + i);
@@ -201,6 +205,7 @@ __device__ __forceinline__ void fast_pair(const rf_row &R, const double *__restr
         double v;
         if (cond_v) {
             v = vgv[e];
+            if (R.flags & RF_ROWF_STYLE_V) v = dsub(v, ddiv(sv[e], tc));
         } else {   // toy_velocity
             const double x0 = dadd(x0v[e], sv[e]);
             v = ddiv(dsub(xv[e], x0), tc);
@@ -348,6 +353,10 @@ extern "C" int rf_tick_solve(const rf_row *rows, int count, int64_t frames, int6
         }
         if (!(R.flags & RF_ROWF_COND_V) && !R.x) {
             set_error("rf_tick_solve: row %d toy velocity needs x", r);
+            return RF_EINVAL;
+        }
+        if ((R.flags & RF_ROWF_STYLE_V) && !(R.t_curr > 0.0)) {
+            set_error("rf_tick_solve: row %d style offset on a velocity needs t_curr > 0", r);
             return RF_EINVAL;
         }
         if (R.neg_kind == RF_NEG_UNCOND && !R.uncond_x0) {

@@ -59,8 +59,8 @@ def _declare(lib):
                                    vp, vp]
     lib.rf_dit_output.restype = vp
     lib.rf_dit_output.argtypes = [vp]
-    lib.rf_attention_bf16.restype = ctypes.c_int
-    lib.rf_attention_bf16.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i64, i64, i64, i64, vp]
+    lib.rf_attention_tc_bf16.restype = ctypes.c_int
+    lib.rf_attention_tc_bf16.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i64, i64, i64, vp]
     lib._dit_declared = True
 
 
@@ -171,6 +171,23 @@ class DiT:
         self.handle = h
         self._cond: dict = {}
         self.out = torch.empty(max_rows, frames, cfg.latent_channels, dtype=torch.float32, device=self.dev)
+        # The handle's workspace, row table, captured graphs and ``out`` are shared mutable
+        # device state: a forward on one stream must not start while an earlier forward
+        # (or the solver reading its velocities) on another stream is still in flight.
+        self._busy = torch.cuda.Event()
+        self._busy_stream = None
+
+    def mark_used(self, stream=None) -> None:
+        """Record that work reading this DiT's buffers was queued on ``stream`` (default:
+        current); the next forward on a different stream waits for it."""
+        stream = stream or torch.cuda.current_stream(self.dev)
+        self._busy.record(stream)
+        self._busy_stream = stream
+
+    def _order_after_previous_use(self) -> None:
+        cur = torch.cuda.current_stream(self.dev)
+        if self._busy_stream is not None and self._busy_stream != cur:
+            cur.wait_event(self._busy)
 
     def __del__(self):
         try:
@@ -179,14 +196,31 @@ class DiT:
         except Exception:
             pass
 
-    def cond_tokens(self, prompt_hash: int) -> torch.Tensor:
-        """Conditioning tokens of a prompt: a seeded stand-in for the text/lyric encoder output."""
-        t = self._cond.get(prompt_hash)
+    def _tokens(self, prompt_hash: int, kind: str) -> torch.Tensor:
+        key = (prompt_hash, kind)
+        t = self._cond.get(key)
         if t is None:
-            g = torch.Generator(device=self.dev).manual_seed(int(prompt_hash) & ((1 << 62) - 1))
+            salt = {"base": 0, "hint": 0x5A17, "timbre": 0x7B1E}[kind]
+            g = torch.Generator(device=self.dev).manual_seed((int(prompt_hash) ^ salt) & ((1 << 62) - 1))
             t = torch.randn(self.cfg.n_cond_tokens, self.cfg.d_model, generator=g, device=self.dev)
+            self._cond[key] = t
+        return t
+
+    def cond_tokens(self, prompt_hash: int, hint: float = 0.0, timbre: float = 0.0) -> torch.Tensor:
+        """Conditioning tokens of a condition: a seeded stand-in for the text / lyric encoder
+        output, plus the audio-hint and timbre embeddings scaled by the condition's
+        strengths (the DiT-side reading of model.py:123-131's
+        x0 = base + 0.45 h hint + 0.45 tau timbre).  Composed once per condition and cached."""
+        key = ("cond", prompt_hash, float(hint), float(timbre))
+        t = self._cond.get(key)
+        if t is None:
+            t = self._tokens(prompt_hash, "base")
+            if hint != 0.0:
+                t = t + (0.45 * hint) * self._tokens(prompt_hash, "hint")
+            if timbre != 0.0:
+                t = t + (0.45 * timbre) * self._tokens(prompt_hash, "timbre")
             t = t.to(torch.bfloat16).contiguous()
-            self._cond[prompt_hash] = t
+            self._cond[key] = t
         return t
 
     def forward(self, xs, ts, conds, out: torch.Tensor = None) -> torch.Tensor:
@@ -195,15 +229,24 @@ class DiT:
         if n > self.max_rows:
             raise ValueError(f"{n} rows > max_rows {self.max_rows}")
         out = self.out if out is None else out
+        self._order_after_previous_use()
         xp = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
         tp = (ctypes.c_float * n)(*[float(t) for t in ts])
         cp = (ctypes.c_void_p * n)(*[c.data_ptr() for c in conds])
         _native.check(self.lib.rf_dit_forward(self.handle, n, xp, tp, cp, out.data_ptr(),
                                               _device.current_stream_handle()), "rf_dit_forward")
+        self.mark_used()
         return out[:n]
 
 
 # ------------------------------------------------- StreamPipeline velocity model --
+@dataclass(frozen=True)
+class _Uncond:
+    prompt_hash: int
+    hint_strength: float = 0.0
+    timbre_strength: float = 0.0
+
+
 @dataclass
 class _Pending:
     xs: list = field(default_factory=list)
@@ -232,10 +275,10 @@ class DiTVelocity:
         n = self.dit.lib.rf_dit_launches(self.dit.handle, self._last_rows) if self._last_rows else 0
         return max(n, 0)
 
-    def _row(self, x, t, prompt_hash) -> int:
+    def _row(self, x, t, cond) -> int:
         self._p.xs.append(x)
         self._p.ts.append(t)
-        self._p.conds.append(self.dit.cond_tokens(prompt_hash))
+        self._p.conds.append(self.dit.cond_tokens(cond.prompt_hash, cond.hint_strength, cond.timbre_strength))
         return len(self._p.xs) - 1
 
     def _ptr(self, idx) -> int:
@@ -247,12 +290,12 @@ class DiTVelocity:
             raise ValueError("DiT batch exceeds max_rows; raise DiT(max_rows=...)")
         row.n_cond = len(conds)
         for j, c in enumerate(conds):
-            row.cond_x0[j] = self._ptr(self._row(slot.x, t_curr, c.prompt_hash))
+            row.cond_x0[j] = self._ptr(self._row(slot.x, t_curr, c))
             if len(conds) > 1:
                 w = c.weight_device()
                 row.cond_w[j] = None if w is None else w.data_ptr()
         if need_uncond:
-            row.uncond_x0 = self._ptr(self._row(slot.x, t_curr, self.uncond_prompt))
+            row.uncond_x0 = self._ptr(self._row(slot.x, t_curr, _Uncond(self.uncond_prompt)))
         row.flags |= _native.RF_ROWF_COND_V | _native.RF_ROWF_UNCOND_V | _native.RF_ROWF_V_F32
 
     def forward(self, pipe) -> None:
@@ -260,3 +303,11 @@ class DiTVelocity:
         if p.xs:
             self._last_rows = len(p.xs)
             self.dit.forward(p.xs, p.ts, p.conds)
+
+    def consumed(self, stream) -> None:
+        """The pipeline queued the solver that reads this tick's velocities on ``stream``."""
+        self.dit.mark_used(stream)
+
+    def reset(self) -> None:
+        """Drop rows prepared for a tick that raised before its forward ran."""
+        self._p = _Pending()

@@ -66,7 +66,9 @@ def mse(a, b) -> float:
         return float("nan")
     out = torch.empty(1, dtype=torch.float64, device=dev)
     lib = _native.load()
-    _native.check(lib.rf_mse(ta.data_ptr(), tb.data_ptr(), n, out.data_ptr(),
+    elems = lib.rf_reduce_workspace_elems(n)
+    scratch = _device.workspace(8 * elems, "reduce", dev)   # this stream's own partials
+    _native.check(lib.rf_mse(ta.data_ptr(), tb.data_ptr(), n, out.data_ptr(), scratch.data_ptr(), elems,
                              _device.current_stream_handle()), "rf_mse")
     return float(out.item())
 

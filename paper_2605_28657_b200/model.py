@@ -29,6 +29,15 @@ HINT_SCALE = 0.45
 TIMBRE_SCALE = 0.45
 
 
+def _frozen_copy(x) -> np.ndarray:
+    if isinstance(x, torch.Tensor):
+        a = x.detach().to("cpu", torch.float64).numpy().copy()
+    else:
+        a = np.array(x, dtype=np.float64, copy=True)
+    a.setflags(write=False)
+    return a
+
+
 @dataclass(frozen=True)
 class ConditionSet:
     """One frozen conditioning bundle (model.py:33-64)."""
@@ -45,6 +54,15 @@ class ConditionSet:
             raise ValueError("hint_strength must be in [0, 1]")
         if not 0.0 <= self.timbre_strength <= 1.0:
             raise ValueError("timbre_strength must be in [0, 1]")
+        # The bundle is frozen in content too: ``source`` / ``weight_curve`` are copied at
+        # construction (read-only host arrays), so the cached content key and device copies
+        # below can never go stale if the caller later mutates the array it passed in.
+        # (The reference re-hashes on every call, model.py:52-61; with an immutable copy the
+        # cached key is the same value.)
+        for name in ("source", "weight_curve"):
+            val = getattr(self, name)
+            if val is not None:
+                object.__setattr__(self, name, _frozen_copy(val))
 
     def content_key(self) -> int:
         """Hash of the conditioning content; keys the noise streams (model.py:53-61)."""

@@ -30,7 +30,7 @@ import torch
 
 from . import _device, _native
 from ._native import RfAdmit, RfEmit, RfRow
-from .latents import NoiseSource, content_hash, fill_normals
+from .latents import NoiseSource, ShapeMismatchError, content_hash, fill_normals
 from .model import UNCOND_PROMPT, ConditionSet, ModelWeights, ToyFlowModel
 from .schedule import ScheduleCache, ScheduleMismatchError, TimestepSchedule, migrate_schedule
 from .solver import (
@@ -279,6 +279,9 @@ class StreamPipeline:
             self._noise = torch.empty((config.depth, 3, T, D), dtype=torch.float64, device=self._dev)
             self._status = torch.zeros(1, dtype=torch.int32, device=self._dev)
             self._stats = torch.empty((2, max(config.depth, 1)), dtype=torch.float64, device=self._dev)
+            # the emit reduction's partials: this pipeline's own (never shared across streams)
+            self._reduce_elems = int(_native.load().rf_reduce_workspace_elems(T * D))
+            self._reduce_scratch = torch.empty(max(self._reduce_elems, 1), dtype=torch.float64, device=self._dev)
         self._stats_host = torch.empty((2, max(config.depth, 1)), dtype=torch.float64).pin_memory()
         self._status_host = torch.empty(1, dtype=torch.int32).pin_memory()
         self.velocity_model = velocity_model   # None: the toy model inside the fused kernel
@@ -407,6 +410,41 @@ class StreamPipeline:
         self._queue.append(sub)
         return sub.submission_id
 
+    # ------------------------------------------------------------- validation
+    def _check_request(self, request: GenerationRequest) -> None:
+        """Host-side checks the reference makes inside the step (every pointer the kernels
+        dereference must cover [T, D] / [T]): a source of the wrong shape raises
+        ShapeMismatchError as ``sde_step`` does (solver.py:300-301), a weight curve of the
+        wrong shape, a negative weight or a zero weight sum raises ValueError as
+        ``blend_conditions`` does (solver.py:217-226).  Checked once per (request, shape):
+        requests are frozen and their arrays are read-only copies (model.py)."""
+        shape = self.config.shape
+        key = ("checked", shape)
+        if request._cache.get(key):  # noqa: SLF001
+            return
+        for c in request.conditions:
+            if c.source is not None and tuple(c.source.shape) != shape:
+                raise ShapeMismatchError(f"source shape {tuple(c.source.shape)} != {shape}")
+        if len(request.conditions) > 1:
+            total = np.zeros(shape[0])
+            for c in request.conditions:
+                w = np.ones(shape[0]) if c.weight_curve is None else c.weight_curve
+                if tuple(w.shape) != (shape[0],):
+                    raise ValueError(f"weight_curve shape {tuple(w.shape)} != ({shape[0]},)")
+                if np.any(w < 0.0):
+                    raise ValueError("condition weights must be nonnegative")
+                total = total + w
+            if np.any(total <= 0.0):
+                raise ValueError("condition weights sum to zero at some frame")
+        curves = request.curves
+        for name in CURVE_FIELDS:
+            val = getattr(curves, name)
+            if val is not None and tuple(val.shape) != (shape[0],):
+                raise ShapeMismatchError(f"{name} must have shape ({shape[0]},), got {tuple(val.shape)}")
+        if curves.x0_target is not None and tuple(np.shape(curves.x0_target)) != shape:
+            raise ShapeMismatchError(f"x0_target shape {tuple(np.shape(curves.x0_target))} != {shape}")
+        request._cache[key] = True  # noqa: SLF001
+
     # ------------------------------------------------------------------- tick
     def tick(self) -> list:
         """Advance every in-flight slot one step; emit finished latents (pipeline.py:372-398)."""
@@ -472,6 +510,8 @@ class StreamPipeline:
     def _step_slots(self, slots: list) -> None:
         """One batched pass over `slots`: noise for every row, then one fused solve."""
         cfg = self.config
+        for slot in slots:
+            self._check_request(slot.request)
         T, D = cfg.shape
         jitter = self.model.perturbation
         draws, rows = [], []
@@ -479,12 +519,16 @@ class StreamPipeline:
             # the DiT's inputs first: its (long) batched forward is launched before the host
             # prepares the solver rows, so that host work overlaps the device work
             rows = [RfRow() for _ in slots]
-            for slot, row in zip(slots, rows):
-                base = slot.request.curves
-                need_uncond = (base.guidance_enabled and
-                               guidance_plan(base.rcfg_mode, slot.state, True)[0] == _native.RF_NEG_UNCOND)
-                self.velocity_model.prepare_row(self, slot, row, float(slot.schedule.sigmas[slot.step]),
-                                                need_uncond)
+            try:
+                for slot, row in zip(slots, rows):
+                    base = slot.request.curves
+                    need_uncond = (base.guidance_enabled and
+                                   guidance_plan(base.rcfg_mode, slot.state, True)[0] == _native.RF_NEG_UNCOND)
+                    self.velocity_model.prepare_row(self, slot, row, float(slot.schedule.sigmas[slot.step]),
+                                                    need_uncond)
+            except BaseException:
+                self.velocity_model.reset()
+                raise
             ev = self._phase_begin("model")
             self.velocity_model.forward(self)
             self._phase_end("model", ev)
@@ -513,6 +557,8 @@ class StreamPipeline:
                     draws.append((slot.rng.key(k, "model"), nbuf[0]))
                     row.noise_model = nbuf[0].data_ptr()
                     row.jitter_t = jitter * t_curr
+            if self.velocity_model is not None and self.weights.version > 0:
+                row.flags |= _native.RF_ROWF_STYLE_V   # set_model_weights on the DiT path
             curve_pointers(row, lambda n: dev[n])
             if base.guidance_enabled:
                 neg_kind, flags = guidance_plan(base.rcfg_mode, slot.state, True)
@@ -553,6 +599,8 @@ class StreamPipeline:
         ev = self._phase_begin("solve")
         _native.check(lib.rf_tick_solve(arr, len(rows), T, D, self.weights.device_offset.data_ptr(),
                                         self._stream.cuda_stream), "rf_tick_solve")
+        if self.velocity_model is not None:
+            self.velocity_model.consumed(self._stream)
         self._phase_end("solve", ev)
         self.launches_last_tick += 1
         self.rows_last_tick = len(rows)
@@ -589,7 +637,8 @@ class StreamPipeline:
         _native.check(lib.rf_emit_stats(
             emits, n, slot.x.numel(), None if last is None else last.data_ptr(),
             None if ref is None else ref.data_ptr(), self._stats[0].data_ptr(),
-            self._stats[1].data_ptr(), self._status.data_ptr(), self._stream.cuda_stream),
+            self._stats[1].data_ptr(), self._status.data_ptr(), self._reduce_scratch.data_ptr(),
+            self._reduce_elems, self._stream.cuda_stream),
             "rf_emit_stats")
         self._phase_end("emit", ev)
         self.launches_last_tick += 2
@@ -664,6 +713,8 @@ class StreamPipeline:
 
     def _init_slots(self, slots: list) -> None:
         """Admission draws + x = n or d*n + (1-d)*source for all new slots (pipeline.py:523-532)."""
+        for slot in slots:
+            self._check_request(slot.request)
         draws, admits = [], (RfAdmit * len(slots))()
         for j, slot in enumerate(slots):
             nbuf = self._noise_buffers(slot)[2]

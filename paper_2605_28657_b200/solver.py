@@ -97,6 +97,17 @@ class CurveSet:
             raise ValueError(f"rcfg_mode must be one of {RCFG_MODES}")
         if self.x0_target_strength is not None and self.x0_target is None:
             raise ValueError("x0_target_strength requires x0_target")
+        # immutable content: array fields are read-only copies, so the device copies cached
+        # below cannot go stale when the caller mutates what it passed in
+        for name in tuple(CURVE_FIELDS) + ("x0_target",):
+            val = getattr(self, name)
+            if val is not None:
+                if isinstance(val, torch.Tensor):
+                    arr = val.detach().to("cpu", torch.float64).numpy().copy()
+                else:
+                    arr = np.array(val, dtype=np.float64, copy=True)
+                arr.setflags(write=False)
+                object.__setattr__(self, name, arr)
 
     def device(self, name: str) -> Optional[torch.Tensor]:
         """Resident device copy of a curve (or of x0_target)."""

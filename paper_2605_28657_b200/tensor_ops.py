@@ -15,13 +15,11 @@ EPI_BF16, EPI_F32, EPI_RESID_GATE, EPI_SWIGLU, EPI_F32_SCALE = 0, 1, 2, 3, 4
 
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor = None, epilogue: int = EPI_BF16,
          gate: torch.Tensor = None, rows_per_batch: int = 1, alpha: float = 1.0, block_n: int = None,
-         pair: bool = False, stream_k: bool = False):
+         pair: bool = False):
     """out = a @ b.T with a [M, K] bf16 and b [N, K] bf16 (K-major), fp32 accumulation.
 
     ``pair``: 256 x block_n tiles on a CTA pair (tcgen05 cta_group::2) instead of 128 x block_n
-    tiles on one CTA; ``stream_k``: every persistent CTA (pair) takes an equal share of the
-    tile-major k-block sequence, split tiles combined in a fixed order (used when the tiles
-    cover every CTA at least once)."""
+    tiles on one CTA."""
     assert a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16 and a.is_cuda and b.is_cuda
     M, K = a.shape
     N = b.shape[0]
@@ -40,6 +38,6 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor = None, epilogue: i
         a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K, a.stride(0), b.stride(0), out.stride(0),
         epilogue, gate.data_ptr() if gate is not None else None,
         gate.stride(0) if gate is not None else 0, rows_per_batch, alpha,
-        -(block_n + 4096 * int(stream_k)) if pair else block_n + 4096 * int(stream_k),
+        -block_n if pair else block_n,
         _device.current_stream_handle()), "rf_gemm_bf16")
     return out
