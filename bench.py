@@ -22,8 +22,12 @@ the ring completes one generation every 2 ticks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank drives its own independent stream (own ring and DiT,
-seed = rank): weak scaling, no data-path collective.
+N > 1: every rank drives its own independent stream (own ring and DiT, seed = rank):
+weak scaling, no data-path collective; the only collective is config 5's sharded long
+decode (NCCL all-gather of the PCM).  Launched under torchrun by the driver; started
+plainly with --gpus N > 1 it re-executes itself under torch.distributed.run with N ranks.
+`--stub` runs the same launch / aggregation / JSON path on the CPU over gloo with a stub
+workload (harness test only: tests/test_bench_harness.py; never a bench number).
 """
 from __future__ import annotations
 
@@ -31,6 +35,7 @@ import argparse
 import json
 import multiprocessing as mp
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -58,7 +63,78 @@ def parse():
     ap.add_argument("--no-toy", action="store_true")
     ap.add_argument("--no-library-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-240s-dit", action="store_true")
+    ap.add_argument("--stub", action="store_true", help="CPU/gloo harness test with a stub workload")
     return ap.parse_args()
+
+
+# ------------------------------------------------------------ launch / ranks -----
+def _free_port() -> int:
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def maybe_respawn(args) -> None:
+    """--gpus N > 1 without a torchrun environment: re-execute under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and exit with its return code."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+
+
+def ranks():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def aggregate(sums, maxes, world, device):
+    """Sum `sums` and max `maxes` over ranks (completions / work add up, times take the
+    slowest rank): the whole-job numbers rank 0 reports."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(list(sums) + list(maxes), dtype=torch.float64, device=device)
+    if world > 1:
+        s, m = t.clone(), t.clone()
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        t = torch.cat([s[:len(sums)], m[len(sums):]])
+    vals = t.tolist()
+    return vals[:len(sums)], vals[len(sums):]
+
+
+def cpu_model() -> str:
+    """The host CPU model (lscpu's "Model name"), reported with every CPU number."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def bench_config():
+    """The workload both arms report (identical dicts, so the driver sees the same config)."""
+    from paper_2605_28657_b200.dit import DiTConfig
+
+    dcfg = DiTConfig()
+    return {"workload": "config 2: ACE-Step-1.5-shape 24-layer DiT (d=2048, 16/8 heads, SwiGLU 6144, random init), "
+                        "60-s latent T=1500 x D=64, ring depth 4, S=8, source present, denoise 1.0, SDE solver; "
+                        "one independent stream per GPU",
+            "frames": T, "channels": D, "depth": DEPTH, "steps_per_generation": STEPS,
+            "dit_params": dcfg.params(), "dit_flops_per_tick": dcfg.flops_per_forward(DEPTH, T),
+            "ring_state": "float64", "dit_compute": "bf16 operands, fp32 accumulate / residual stream"}
 
 
 def peaks():
@@ -309,9 +385,9 @@ def run_ours(args):
     import paper_2605_28657_b200 as rf
     from paper_2605_28657_b200 import dit as dit_mod
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = ranks()
+    if torch.cuda.device_count() < local + 1:
+        sys.exit(f"bench.py: rank {rank} needs cuda:{local} but only {torch.cuda.device_count()} GPU(s) are visible")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -384,6 +460,7 @@ def run_ours(args):
             ev.append((a, b))
     torch.cuda.synchronize()
     decode_ms = sorted(a.elapsed_time(b) for a, b in ev)[len(ev) // 2]
+    weights_keep = model.weights
     del pipe, model
     torch.cuda.empty_cache()
 
@@ -399,6 +476,11 @@ def run_ours(args):
         library["what"] = ("config-2 DiT forward (4 rows) in stock PyTorch: cuBLAS bf16 GEMMs, SDPA attention, "
                            "torch elementwise norms/RoPE/SwiGLU, one CUDA graph (tools/dit_torch_baseline.py); "
                            "native = this repo's tcgen05 forward on the same weights")
+
+    # ---------------- config 5 generation: the DiT tick at 240 s ----------------
+    dit240 = None if args.no_240s_dit else dit_tick_240s(rf, dit_mod, weights_keep, rank, flush, bf16_sust)
+    del weights_keep
+    torch.cuda.empty_cache()
 
     # ---------------- toy-velocity leg (the reference's own model) ----------------
     toy = None
@@ -421,33 +503,26 @@ def run_ours(args):
                "gpu_launches": t_launch, "dtype": "f64",
                "note": "same ring and solver with ToyFlowModel velocities (bit-exact vs the reference)"}
 
-    # ---- aggregate over ranks ----
-    tot = torch.tensor([completions, dev_ms, e2e_done, e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        s, m = tot.clone(), tot.clone()
-        dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX)
-        completions_all, dev_ms_max, e2e_all, e2e_max = s[0].item(), m[1].item(), s[2].item(), m[3].item()
-    else:
-        completions_all, dev_ms_max, e2e_all, e2e_max = completions, dev_ms, e2e_done, e2e_s
+    # ---- aggregate over ranks (sums of work, max of times) ----
+    (completions_all, e2e_all, flops_all, launches_all), (dev_ms_max, e2e_max, model_ms_max) = aggregate(
+        [completions, e2e_done, dit_flops * args.steps, launches],
+        [dev_ms, e2e_s, phase_ms["model"] * args.steps], world, dev)
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
     value = completions_all / (dev_ms_max * 1e-3)
+    # whole-job tensor throughput of the forwards against world x the sustained peak
+    agg_tflops = flops_all / (model_ms_max * 1e-3) / 1e12
+    traffic_warm, traffic_cold = forward_traffic()
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "config 2: ACE-Step-1.5-shape 24-layer DiT (d=2048, 16/8 heads, SwiGLU 6144, "
-                               "random init), 60-s latent T=1500 x D=64, ring depth 4, S=8, source present, "
-                               "denoise 1.0; one independent stream per GPU",
-                   "frames": T, "channels": D, "depth": DEPTH, "steps_per_generation": STEPS,
-                   "dit_params": dcfg.params(), "dit_flops_per_tick": dit_flops,
-                   "ring_state": "float64", "dit_compute": "bf16 operands, fp32 accumulate/residual",
-                   "l2": "flushed (256 MiB write) between timed ticks, outside the events",
-                   "completions_timed": int(completions_all)},
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded latents, random-init DiT)",
+        "config": bench_config(),
+        "l2": "flushed (256 MiB write) between timed ticks, outside the events",
+        "completions_timed": int(completions_all),
         "e2e": {"value": round(e2e_all / e2e_max, 3), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
                 "note": "wall clock through StreamPipeline: a host shared-curve write every tick (value flips every 8), "
@@ -458,14 +533,15 @@ def run_ours(args):
         "decode_240s": long_decode,
         "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
         "roofline": {"bound": "tensor", "kernel": "dit_forward (tcgen05 GEMMs + attention + norms, one launch set)",
-                     "achieved": round(dit_tflops, 1), "peak": bf16_sust, "unit": "TFLOP/s",
-                     "frac": round(dit_tflops / bf16_sust, 4), "traffic": forward_traffic()[0],
+                     "achieved": round(agg_tflops, 1), "peak": round(world * bf16_sust, 1), "unit": "TFLOP/s",
+                     "frac": round(agg_tflops / (world * bf16_sust), 4), "traffic": traffic_warm,
                      "traffic_note": "DRAM read+write bytes of one forward (sum over its launches) from the "
                                      "committed ncu launch list profiles/r1_dit_forward_traffic.json, "
-                                     f"--cache-control none; cold-cache sum {forward_traffic()[1]}",
+                                     f"--cache-control none; cold-cache sum {traffic_cold}",
                      "algorithmic_flops_per_launch": dit_flops,
-                     "peak_source": f"{peak_src} bf16 sustained (burst {bf16_burst})"},
-        "gpu_launches": int(launches),
+                     "peak_source": f"{peak_src} bf16 sustained x {world} GPU(s) (burst {bf16_burst} per GPU)",
+                     "per_gpu_frac": round(agg_tflops / world / bf16_sust, 4)},
+        "gpu_launches": int(launches_all),
         "clocks": clocks,
     }
     if toy is not None:
@@ -474,12 +550,73 @@ def run_ours(args):
         line["library_baseline"] = library
     if configs is not None:
         line["other_configs"] = configs
+    if dit240 is not None:
+        line["config5_dit_tick"] = dit240
     if not args.no_cpu_baseline:
         # the same workload (config 2 with the DiT) on the box's host cores, bounded sample
         line["cpu_baseline"] = cpu_dit_baseline(args.cpu_seconds, os.cpu_count() or 1)
         # and the reference's own toy model on one core (its CPU speed on its only model)
         line["cpu_baseline_toy_model"] = cpu_baseline(args.cpu_seconds, processes=1)
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def dit_tick_240s(rf, dit_mod, weights, rank, flush, bf16_sust, ticks=16):
+    """Config 5's generation side: the DiT tick on a 240-s latent (T=6000 -> 3000 tokens),
+    depth 4, S=8, same weights; device time per tick as for `value` (PAPER.md:322 quotes
+    the production decoder at B=8 for this length)."""
+    import torch
+
+    frames = 6000
+    m = dit_mod.DiT(dit_mod.DiTConfig(), frames=frames, max_rows=DEPTH, weights=weights)
+    import scenarios
+
+    src = scenarios.keyed(rank, "bench-source-240", (frames, D))
+    req = rf.GenerationRequest(conditions=(rf.ConditionSet(prompt_hash=rf.content_hash("bench", "bench prompt"),
+                                                           source=src),))
+    p = rf.StreamPipeline(rf.PipelineConfig(depth=DEPTH, steps=STEPS, frames=frames, channels=D, seed=rank),
+                          request=req, velocity_model=dit_mod.DiTVelocity(m))
+    fill = 0
+    while fill < 4 * STEPS and not p.tick():
+        fill += 1
+    for _ in range(3):
+        p.tick()
+    torch.cuda.synchronize()
+    ms, done, _, ph = timed_ticks(p, ticks, flush, p.stream, phases=True)
+    flops = dit_mod.DiTConfig().flops_per_forward(DEPTH, frames)
+    tf = flops / (ph["model"] * 1e-3) / 1e12
+    del p, m
+    torch.cuda.empty_cache()
+    return {"workload": "config 5 generation: 240-s latent T=6000 x D=64 (3000 DiT tokens), depth 4, S=8, DiT",
+            "value": round(done / (ms * 1e-3), 3), "unit": UNIT, "ms_per_step": round(ms / ticks, 3),
+            "ticks": ticks, "completions": done, "phase_ms": {k: round(v, 3) for k, v in ph.items()},
+            "dit_flops_per_tick": flops, "dit_tflops": round(tf, 1), "frac_of_sustained_peak": round(tf / bf16_sust, 4)}
+
+
+def run_stub(args):
+    """Harness test on the CPU: the torchrun launch, rank setup, aggregation and JSON line
+    of the real arm over gloo with a stub workload (each rank 'completes' one generation
+    every other step).  Never a bench number: impl 'stub'."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = ranks()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    done = 0
+    for k in range(args.warmup + args.steps):
+        if k >= args.warmup and k % 2:
+            done += 1
+    wall_ms = (time.perf_counter() - t0) * 1e3 + 1e-3
+    (done_all, ranks_seen), (ms_max,) = aggregate([done, 1], [wall_ms], world, torch.device("cpu"))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "impl": "stub", "value": done_all / (ms_max * 1e-3), "unit": UNIT,
+                          "n_gpus": world, "ranks_reporting": int(ranks_seen), "completions_timed": int(done_all),
+                          "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                          "data": "stub workload on CPU/gloo: harness test only, not a measurement"}), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -516,7 +653,7 @@ def cpu_baseline(seconds, processes=1):
     done = sum(r[0] for r in res)
     ticks = sum(r[1] for r in res)
     wall = max(r[2] for r in res)
-    return {"value": round(done / wall, 3), "unit": UNIT, "cores": processes, "kind": "port",
+    return {"value": round(done / wall, 3), "unit": UNIT, "cores": processes, "kind": "port", "cpu_model": cpu_model(),
             "sample": f"oracle/ringflow_np.py StreamPipeline restatement (toy velocity model, the reference's "
                       f"only model), config-2 shape (T=1500, D=64, depth 4, S=8), {processes} independent "
                       f"stream(s), {ticks} warm ticks after {4 * STEPS} warmup, {wall:.1f} s wall, float64 numpy, "
@@ -555,12 +692,14 @@ def cpu_dit_baseline(seconds, threads, max_ticks=None):
         ticks += 1
     wall = time.perf_counter() - t0
     return {"value": round(row_steps / STEPS / wall, 5), "unit": UNIT, "cores": threads, "kind": "port",
-            "ticks": ticks,
+            "cpu_model": cpu_model(), "ticks": ticks,
             "sample": f"config 2 on the host CPU: oracle/ringflow_np.py tick (the reference's algorithm, float64 "
                       f"numpy) with the ACE-Step-shape DiT (oracle/dit_fp32.py, torch CPU, bf16 GEMM/attention "
                       f"operands with fp32 accumulation, {threads} threads) in "
                       f"the model slot; {ticks} steady-state tick(s) ({row_steps} DiT row forwards + SDE steps) "
-                      f"in {wall:.1f} s after the ring was filled; completions/s = row-steps / S / wall"}
+                      f"in {wall:.1f} s after the ring was filled; completions/s = row-steps / S / wall; "
+                      f"one DiT forward per ring row per tick (the reference's per-slot model loop, "
+                      f"pipeline.py:449-464), rows not batched"}
 
 
 def run_reference(args):
@@ -574,12 +713,11 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": base["ticks"], "steps_requested": args.steps, "warmup": args.warmup, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 DiT / f64 tick", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded latents, random-init DiT)",
         "impl": "reference",
-        "config": {"workload": "config 2: ACE-Step-1.5-shape 24-layer DiT (d=2048, 16/8 heads, SwiGLU 6144, "
-                               "random init), 60-s latent T=1500 x D=64, ring depth 4, S=8, source present, "
-                               "denoise 1.0; the reference's tick on the host CPU (oracle port) with the DiT "
-                               "(torch CPU, bf16 operands, all host threads) in its model slot"},
+        "config": bench_config(),
+        "arm": "the reference's tick on the host CPU (oracle port, float64 numpy) with the DiT (torch CPU, bf16 "
+               "operands, all host threads) in its model slot",
         "cpu_baseline": base,
         "toy_model": {**toy, "note": "the reference's own ToyFlowModel at config-2 shape, one stream per host "
                                      "core: the reference's CPU speed on its only model"},
@@ -599,7 +737,10 @@ def refuse_tuning_env():
 if __name__ == "__main__":
     refuse_tuning_env()
     a = parse()
+    maybe_respawn(a)
     if a.impl == "reference":
         run_reference(a)
+    elif a.stub:
+        run_stub(a)
     else:
         run_ours(a)

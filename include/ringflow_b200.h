@@ -218,6 +218,12 @@ int rf_gemm_bf16(const void *A, const void *B, void *out, int64_t M, int64_t N, 
 int rf_attention_tc_bf16(const void *q, const void *k, const void *vt, void *out, int32_t batch, int32_t n_q,
                          int32_t n_k, int32_t n_k_pad, int32_t heads, int32_t kv_heads, int64_t ldq, int64_t ldk,
                          int64_t ldo, void *stream);
+/* The same with the kernel for > 128 keys chosen explicitly (benchmarks / tests; the DiT
+ * forward always uses kernel 0, the default): 0 = default, 1 = 64-key tiles with
+ * double-buffered scores, one head per CTA (non-persistent). */
+int rf_attention_tc_bf16_kernel(int32_t kernel, const void *q, const void *k, const void *vt, void *out,
+                                int32_t batch, int32_t n_q, int32_t n_k, int32_t n_k_pad, int32_t heads,
+                                int32_t kv_heads, int64_t ldq, int64_t ldk, int64_t ldo, void *stream);
 
 /* --------------------------------------------------- ACE-Step-shape DiT (A8) ------
  * The velocity model that replaces the reference's ToyFlowModel for BASELINE configs

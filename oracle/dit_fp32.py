@@ -36,13 +36,17 @@ def _rope(x, cos, sin):
     return torch.stack([y0, y1], -1).flatten(-2)
 
 
-def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float(), bf16_matmul=False):
+def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float(), bf16_matmul=False, pure=False):
     """The DiT in fp32.  cfg: DiTConfig; W: weights with the DiTWeights attribute names
     (f maps a stored weight to the fp32 tensor used); xs: [frames, C] latents; ts: per-row
     timesteps; conds: [n_cond_tokens, d] conditioning tokens.  Returns [B, frames, C].
     bf16_matmul: GEMM and attention operands in bf16 (weights stored bf16; products
     accumulated in fp32 by the backend, outputs rounded to bf16) -- the CPU timing arm's
-    fast path (AMX); the oracle itself is fp32."""
+    fast path (AMX); the oracle itself is fp32.
+    pure: no bf16 rounding points at all -- the latent, timestep features, every activation
+    and GEMM operand stay fp32 (the weights and conditioning tokens are bf16-VALUED inputs
+    of the model, upcast exactly); with TF32 off this is the true fp32 network, the
+    reference the bf16-vs-fp32 drift of the GPU forward is measured against."""
     if bf16_matmul:
         matmul = lambda a, w: (a.bfloat16() @ w.T).float()  # noqa: E731
     else:
@@ -51,16 +55,17 @@ def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float
     B, T, C = len(xs), frames, cfg.latent_channels
     N, d = T // cfg.patch, cfg.d_model
     H, Hk, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+    bfr = (lambda t: t) if pure else (lambda t: t.bfloat16().float())  # noqa: E731
     x = torch.stack([xx.float() for xx in xs]).reshape(B, N, cfg.in_dim)
-    x = x.bfloat16().float()
+    x = bfr(x)
     dev = x.device
     half = cfg.freq_dim // 2
     freqs = torch.exp(-math.log(10000.0) * torch.arange(half, device=dev, dtype=torch.float32) / half)
     args = 1000.0 * torch.tensor([float(t) for t in ts], device=dev)[:, None] * freqs[None]
-    tf = torch.cat([torch.cos(args), torch.sin(args)], -1).bfloat16().float()
+    tf = bfr(torch.cat([torch.cos(args), torch.sin(args)], -1))
     silu = torch.nn.functional.silu
-    temb = matmul(silu(matmul(tf, W.w_t1)).bfloat16().float(), W.w_t2)
-    st = silu(temb).bfloat16().float()
+    temb = matmul(bfr(silu(matmul(tf, W.w_t1))), W.w_t2)
+    st = bfr(silu(temb))
     mod = matmul(st, W.w_ada)                       # [B, 6d]
     fmod = matmul(st, W.w_final_ada)                # [B, 2d]
     h = matmul(x, W.w_in)                           # [B, N, d]
@@ -70,7 +75,6 @@ def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float
     ang = pos[:, None] * inv[None]
     cos, sin = torch.cos(ang).float()[None, :, None, :], torch.sin(ang).float()[None, :, None, :]
     cond = torch.stack([c.float() for c in conds])  # [B, Nc, d]
-    bfr = lambda t: t.bfloat16().float()  # noqa: E731
     L = cfg.n_layers if layers is None else layers
     for l in range(L):
         m = mod + W.ada_table[l][None]
@@ -107,14 +111,41 @@ def forward_fp32(cfg, W, frames, xs, ts, conds, layers=None, f=lambda w: w.float
     return v.reshape(B, T, C)
 
 
-def reference_forward(dit, xs, ts, conds, layers: int = None) -> torch.Tensor:
-    """forward_fp32 on a (GPU) ``paper_2605_28657_b200.dit.DiT``'s own bf16 weights, no TF32."""
-    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+def reference_forward(dit, xs, ts, conds, layers: int = None, pure: bool = False) -> torch.Tensor:
+    """forward_fp32 on a (GPU) ``paper_2605_28657_b200.dit.DiT``'s own bf16 weights, no TF32
+    (pure=True: no bf16 rounding points anywhere -- the true fp32 network)."""
+    prev = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32)
     torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
     try:
-        return forward_fp32(dit.cfg, dit.weights, dit.frames, xs, ts, conds, layers)
+        with torch.no_grad():
+            return forward_fp32(dit.cfg, dit.weights, dit.frames, xs, ts, conds, layers, pure=pure)
     finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+        torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = prev
+
+
+class Fp32DiTVelocity:
+    """The pure-fp32 DiT (``reference_forward(pure=True)`` on a GPU ``DiT``'s own weights and
+    conditioning tokens) as the oracle pipeline's model (``oracle/ringflow_np.py``:
+    ``Pipeline.model.velocity(x, t, cond, style, seed, stream, step)``): the trajectory
+    reference for the bf16 GPU DiT.  The same conditioning as ``DiTVelocity`` (prompt tokens
+    + 0.45 h hint + 0.45 tau timbre embeddings; the unconditional branch is prompt 0) and the
+    same shared style offset in x0 space (v - style / t); no model jitter (the DiT path has
+    none).  Runs on the GPU in fp32 for speed only -- it is the checker, never the product.
+    ``log`` keeps (t, velocity) of every call when ``record`` is set."""
+
+    def __init__(self, dit, record: bool = False):
+        self.dit, self.record, self.log = dit, record, []
+
+    def velocity(self, x, t, c, style, seed, stream, step):
+        cond = self.dit.cond_tokens(c.prompt_hash, c.hint, c.timbre)
+        xt = torch.from_numpy(np.ascontiguousarray(x)).to(self.dit.dev)
+        v = reference_forward(self.dit, [xt], [t], [cond], pure=True)[0].double().cpu().numpy()
+        if np.any(style != 0.0):
+            v = v - style / t
+        if self.record:
+            self.log.append((float(t), v))
+        return v
 
 
 class CpuDiTVelocity:

@@ -399,6 +399,14 @@ class Pipeline:
         self.tick_index += 1
         return out
 
+    def snapshot(self):  # pipeline.py:289-304 (PipelineSnapshot / SlotView)
+        from types import SimpleNamespace as NS
+
+        slots = tuple(None if s is None else NS(denoise=s.denoise, step=s.st.step, schedule_id=s.sched.schedule_id)
+                      for s in self.slots)
+        return NS(slots=slots, queue_depth=len(self.queue), mode=self.mode, tick=self.tick_index,
+                  denoise=self.denoise, denoise_values=lambda: {v.denoise for v in slots if v is not None})
+
     def curves_of(self, s):  # pipeline.py:415-422
         c = dict(s.req.curves)
         c["x0_target"] = s.req.x0_target

@@ -88,7 +88,7 @@ EXPORTS = (
     "rf_tick_solve", "rf_x0_compose", "rf_admit_init", "rf_emit_stats", "rf_reduce_workspace_elems",
     "rf_decode_workspace_bytes", "rf_decode_window", "rf_encode_frames", "rf_mse", "rf_gemm_bf16",
     "rf_dit_workspace_bytes", "rf_dit_create", "rf_dit_destroy", "rf_dit_forward",
-    "rf_dit_output", "rf_attention_tc_bf16",
+    "rf_dit_output", "rf_attention_tc_bf16", "rf_attention_tc_bf16_kernel",
 )
 
 _lock = threading.Lock()

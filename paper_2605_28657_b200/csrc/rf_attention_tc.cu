@@ -691,13 +691,20 @@ static int launch_fa64(const AttnPlan &p, void *out, int64_t ldo, int B, float s
     return RF_OK;
 }
 
+// Kernel choice for > 128 keys (development A/B through rf_attention_tc_bf16_kernel only;
+// the DiT forward always takes the default).
+static int g_self_kernel = 0;
+
 int attn_run(const AttnPlan &p, void *out, int64_t ldo, int B, cudaStream_t st) {
     const float sc = 1.4426950408889634f / sqrtf(128.f);
     // one key tile (cross-attention to <= 128 conditioning tokens): one head per CTA, two
     // CTAs per SM; longer key ranges: 64-key tiles with double-buffered scores, one head per
-    // CTA, two CTAs per SM
+    // CTA, two CTAs per SM (a 128-key-tile single-buffered variant measured slower: 33.2 vs
+    // 31.1 us at config 2, 289 vs 269 us at 3000 tokens; profiles/r2_attention.txt)
     if (p.Nk <= kTcRows) return launch_fa<1, 1>(p, out, ldo, B, sc, st);
-    return launch_fa64<1>(p, out, ldo, B, sc, st);
+    switch (g_self_kernel) {
+        default: return launch_fa64<1>(p, out, ldo, B, sc, st);
+    }
 }
 
 }  // namespace rf
@@ -709,6 +716,27 @@ using namespace rf;
 extern "C" int rf_attn_set_trace(void *buf) {
     unsigned long long *p = (unsigned long long *)buf;
     return cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)) == cudaSuccess ? RF_OK : RF_ECUDA;
+}
+
+// Development entry (not used by the forward): the same attention with the kernel for > 128
+// keys chosen explicitly (0 = the forward's default).
+extern "C" int rf_attention_tc_bf16_kernel(int32_t kernel, const void *q, const void *k, const void *vt, void *out,
+                                           int32_t batch, int32_t n_q, int32_t n_k, int32_t n_k_pad, int32_t heads,
+                                           int32_t kv_heads, int64_t ldq, int64_t ldk, int64_t ldo, void *stream) {
+    if (!q || !k || !vt || !out || batch < 1 || n_q < 1 || n_k < 1 || heads < 1 || kv_heads < 1 || kernel < 0 ||
+        kernel > 1) {
+        set_error("rf_attention_tc_bf16_kernel: bad arguments");
+        return RF_EINVAL;
+    }
+    AttnPlan p;
+    int rc = attn_plan(&p, q, ldq, (int64_t)heads * 128, k, ldk, (int64_t)kv_heads * 128, vt, batch, n_q, n_k,
+                       n_k_pad, heads, kv_heads);
+    if (rc) return rc;
+    const int keep = g_self_kernel;
+    g_self_kernel = kernel;
+    rc = attn_run(p, out, ldo, batch, (cudaStream_t)stream);
+    g_self_kernel = keep;
+    return rc;
 }
 
 extern "C" int rf_attention_tc_bf16(const void *q, const void *k, const void *vt, void *out, int32_t batch,

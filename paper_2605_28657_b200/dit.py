@@ -172,25 +172,36 @@ class DiT:
         self._cond: dict = {}
         self.out = torch.empty(max_rows, frames, cfg.latent_channels, dtype=torch.float32, device=self.dev)
         # The handle's workspace, row table, captured graphs and ``out`` are shared mutable
-        # device state: a forward on one stream must not start while an earlier forward
-        # (or the solver reading its velocities) on another stream is still in flight.
-        self._busy = torch.cuda.Event()
-        self._busy_stream = None
+        # device state: a forward on one stream must not start while earlier work using them
+        # (a forward, or a solver reading the velocities) on another stream is in flight.
+        # One event per stream that used them; the allocator is told about every such
+        # stream (record_stream), so their memory is not reused before that work is done.
+        self._busy: dict = {}
+        # weights, tables and the handle were initialised on the creating stream: complete
+        # them before any other stream can touch them
+        torch.cuda.current_stream(self.dev).synchronize()
 
     def mark_used(self, stream=None) -> None:
         """Record that work reading this DiT's buffers was queued on ``stream`` (default:
         current); the next forward on a different stream waits for it."""
         stream = stream or torch.cuda.current_stream(self.dev)
-        self._busy.record(stream)
-        self._busy_stream = stream
+        ev = self._busy.get(stream)
+        if ev is None:
+            self.workspace.record_stream(stream)
+            self.out.record_stream(stream)
+            ev = self._busy[stream] = torch.cuda.Event()
+        ev.record(stream)
 
     def _order_after_previous_use(self) -> None:
         cur = torch.cuda.current_stream(self.dev)
-        if self._busy_stream is not None and self._busy_stream != cur:
-            cur.wait_event(self._busy)
+        for stream, ev in self._busy.items():
+            if stream != cur:
+                cur.wait_event(ev)
 
     def __del__(self):
         try:
+            for ev in getattr(self, "_busy", {}).values():
+                ev.synchronize()   # in-flight graph replays still use the handle's buffers
             if getattr(self, "handle", None):
                 self.lib.rf_dit_destroy(self.handle)
         except Exception:
@@ -220,6 +231,9 @@ class DiT:
             if timbre != 0.0:
                 t = t + (0.45 * timbre) * self._tokens(prompt_hash, "timbre")
             t = t.to(torch.bfloat16).contiguous()
+            # cached tokens are read from any stream (every pipeline sharing this DiT):
+            # finish creating them before handing them out
+            torch.cuda.current_stream(self.dev).synchronize()
             self._cond[key] = t
         return t
 

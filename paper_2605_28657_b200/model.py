@@ -177,6 +177,8 @@ class ToyFlowModel:
             cond.hint_strength * HINT_SCALE, timbre.data_ptr() if timbre is not None else None,
             cond.timbre_strength * TIMBRE_SCALE, None, out.numel(), _device.current_stream_handle()),
             "rf_x0_compose")
+        # cached and read from any pipeline's stream: complete it before handing it out
+        torch.cuda.current_stream().synchronize()
         self._partials[key] = out
         return out
 

@@ -54,6 +54,7 @@ __all__ = [
     "SlotView",
     "PipelineSnapshot",
     "StreamPipeline",
+    "StreamGroup",
 ]
 
 MODES = ("per-slot", "global-reset", "migration")
@@ -449,30 +450,38 @@ class StreamPipeline:
     def tick(self) -> list:
         """Advance every in-flight slot one step; emit finished latents (pipeline.py:372-398)."""
         with self._lock, torch.cuda.stream(self._stream):
-            self.launches_last_tick = 0
-            if self.mode == "migration":
-                self._migration_pass()
-            if self.mode == "global-reset" and self.denoise != self._prev_tick_denoise:
-                self._slots = [None] * self.config.depth
-                self._warmup_left = self.config.depth
-                self._last_admit = None
-            active = [s for s in self._slots if s is not None]
-            self.last_timesteps = [(s.schedule.sigmas[s.step], s.schedule.schedule_id) for s in active]
+            active = self._tick_begin()
             if active:
                 self._step_slots(active)
-            finished = [(i, s) for i, s in enumerate(self._slots)
-                        if s is not None and s.step >= self.config.steps]
-            # emit: the statistics kernel and its read-back are queued, the finished slots
-            # are refilled (admission kernels queued behind them), and only then does the
-            # host wait for the device to build the records
-            pending = self._emit_launch(finished) if finished else None
-            for i, _ in finished:
-                self._slots[i] = None
-            self._refill()
-            records = self._emit_finish(finished, *pending) if finished else []
-            self._prev_tick_denoise = self.denoise
-            self._tick_index += 1
-            return records
+            return self._tick_end()
+
+    def _tick_begin(self) -> list:
+        """Mode pre-pass and the active slots of this tick (pipeline.py:372-385)."""
+        self.launches_last_tick = 0
+        if self.mode == "migration":
+            self._migration_pass()
+        if self.mode == "global-reset" and self.denoise != self._prev_tick_denoise:
+            self._slots = [None] * self.config.depth
+            self._warmup_left = self.config.depth
+            self._last_admit = None
+        active = [s for s in self._slots if s is not None]
+        self.last_timesteps = [(s.schedule.sigmas[s.step], s.schedule.schedule_id) for s in active]
+        return active
+
+    def _tick_end(self) -> list:
+        """Emit finished slots, refill, advance the tick counter (pipeline.py:386-398)."""
+        finished = [(i, s) for i, s in enumerate(self._slots) if s is not None and s.step >= self.config.steps]
+        # emit: the statistics kernel and its read-back are queued, the finished slots are
+        # refilled (admission kernels queued behind them), and only then does the host wait
+        # for the device to build the records
+        pending = self._emit_launch(finished) if finished else None
+        for i, _ in finished:
+            self._slots[i] = None
+        self._refill()
+        records = self._emit_finish(finished, *pending) if finished else []
+        self._prev_tick_denoise = self.denoise
+        self._tick_index += 1
+        return records
 
     def _migration_pass(self) -> None:
         target = self.cache.get(self.denoise, self.config.steps, self.config.shift)
@@ -507,32 +516,41 @@ class StreamPipeline:
             host["x0_target_strength"] = dev["x0_target_strength"] = None
         return host, dev, base
 
-    def _step_slots(self, slots: list) -> None:
-        """One batched pass over `slots`: noise for every row, then one fused solve."""
+    def _model_rows(self, slots: list) -> list:
+        """The velocity model's rows of this tick (one per slot x condition, + uncond rows),
+        queued on the model; returns the solver row descriptors they feed."""
+        rows = [RfRow() for _ in slots]
+        try:
+            for slot, row in zip(slots, rows):
+                base = slot.request.curves
+                need_uncond = (base.guidance_enabled and
+                               guidance_plan(base.rcfg_mode, slot.state, True)[0] == _native.RF_NEG_UNCOND)
+                self.velocity_model.prepare_row(self, slot, row, float(slot.schedule.sigmas[slot.step]),
+                                                need_uncond)
+        except BaseException:
+            self.velocity_model.reset()
+            raise
+        return rows
+
+    def _step_slots(self, slots: list, rows: Optional[list] = None) -> None:
+        """One batched pass over `slots`: noise for every row, then one fused solve.
+        rows: model rows already prepared and forwarded by a ``StreamGroup``."""
         cfg = self.config
         for slot in slots:
             self._check_request(slot.request)
         T, D = cfg.shape
         jitter = self.model.perturbation
-        draws, rows = [], []
-        if self.velocity_model is not None:
+        draws = []
+        if self.velocity_model is not None and rows is None:
             # the DiT's inputs first: its (long) batched forward is launched before the host
             # prepares the solver rows, so that host work overlaps the device work
-            rows = [RfRow() for _ in slots]
-            try:
-                for slot, row in zip(slots, rows):
-                    base = slot.request.curves
-                    need_uncond = (base.guidance_enabled and
-                                   guidance_plan(base.rcfg_mode, slot.state, True)[0] == _native.RF_NEG_UNCOND)
-                    self.velocity_model.prepare_row(self, slot, row, float(slot.schedule.sigmas[slot.step]),
-                                                    need_uncond)
-            except BaseException:
-                self.velocity_model.reset()
-                raise
+            rows = self._model_rows(slots)
             ev = self._phase_begin("model")
             self.velocity_model.forward(self)
             self._phase_end("model", ev)
             self.launches_last_tick += getattr(self.velocity_model, "launches_per_forward", 0)
+        elif rows is None:
+            rows = []
         for i, slot in enumerate(slots):
             k = slot.step
             t_curr = float(slot.schedule.sigmas[k])
@@ -751,3 +769,64 @@ class StreamPipeline:
                 self._step_slots([slot])
             out = x.cpu().numpy()
             return out
+
+
+class StreamGroup:
+    """Co-resident streams on one GPU ticked together with ONE batched DiT forward
+    ("rows of several co-resident streams may be batched into one DiT
+    forward").  Every pipeline keeps its own ring, registry, schedules and CUDA stream;
+    per tick the group gathers every pipeline's model rows (their slots x conditions, +
+    unconditional rows), runs one forward on the group's stream, then each pipeline solves,
+    emits and refills on its own stream.  DiT rows are independent (no cross-row reduction
+    in any kernel), so each stream's completions are bit-identical to ticking it alone.
+
+    All pipelines must share ``velocity_model`` (one ``DiTVelocity`` whose DiT has
+    ``max_rows`` >= the rows of all streams together)."""
+
+    def __init__(self, pipelines: list):
+        if not pipelines:
+            raise ValueError("a stream group needs at least one pipeline")
+        vm = pipelines[0].velocity_model
+        if vm is None or any(p.velocity_model is not vm for p in pipelines):
+            raise ValueError("the pipelines of a group must share one DiT velocity model")
+        self.pipelines = list(pipelines)
+        self.velocity_model = vm
+        self._stream = torch.cuda.Stream(pipelines[0]._dev)  # noqa: SLF001
+
+    @property
+    def stream(self) -> torch.cuda.Stream:
+        return self._stream
+
+    def tick(self) -> list:
+        """One tick of every stream; returns one list of CompletionRecords per pipeline."""
+        pipes = self.pipelines
+        for p in pipes:
+            p._lock.acquire()  # noqa: SLF001
+        try:
+            begun = []
+            for p in pipes:
+                with torch.cuda.stream(p.stream):
+                    active = p._tick_begin()  # noqa: SLF001
+                    rows = p._model_rows(active) if active else []  # noqa: SLF001
+                begun.append((active, rows))
+            if any(a for a, _ in begun):
+                for p in pipes:   # the forward reads every ring's latents as of its last step
+                    self._stream.wait_stream(p.stream)
+                with torch.cuda.stream(self._stream):
+                    self.velocity_model.forward(None)
+                done = torch.cuda.Event()
+                done.record(self._stream)
+            out, counted = [], False
+            for p, (active, rows) in zip(pipes, begun):
+                with torch.cuda.stream(p.stream):
+                    if active:
+                        p.stream.wait_event(done)
+                        if not counted:   # the shared forward's kernels, counted once
+                            p.launches_last_tick += getattr(self.velocity_model, "launches_per_forward", 0)
+                            counted = True
+                        p._step_slots(active, rows)  # noqa: SLF001
+                    out.append(p._tick_end())  # noqa: SLF001
+            return out
+        finally:
+            for p in pipes:
+                p._lock.release()  # noqa: SLF001

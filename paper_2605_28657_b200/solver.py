@@ -128,6 +128,20 @@ def make_curves(frames: int, x0_target=None, guidance_enabled: bool = False,
                     **clamped)
 
 
+class DeviceState(torch.Tensor):
+    """A device buffer of solver state that converts to a host numpy array on demand
+    (``np.asarray(state.residual)``), as the reference's numpy state does (solver.py:118-134);
+    the kernels use it in place on the device."""
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.detach().as_subclass(torch.Tensor).cpu().numpy()
+        return a if dtype is None else a.astype(dtype, copy=False)
+
+
+def _state_buffer(like) -> torch.Tensor:
+    return torch.empty_like(like).as_subclass(DeviceState)
+
+
 @dataclass
 class StepState:
     """Slot-owned solver scratch (solver.py:118-134); buffers live on the device."""
@@ -178,12 +192,12 @@ def prepare_guidance_state(row: _native.RfRow, state: StepState, curves_apg_pres
                            like: torch.Tensor) -> None:
     """Allocate the slot's guidance buffers the kernel will write and wire pointers."""
     if row.flags & _native.RF_ROWF_WRITE_RESIDUAL:
-        state.residual = torch.empty_like(like)
+        state.residual = _state_buffer(like)
     if row.flags & _native.RF_ROWF_WRITE_PREV and state.prev_positive is None:
-        state.prev_positive = torch.empty_like(like)
+        state.prev_positive = _state_buffer(like)
     if curves_apg_present:
         if state.momentum is None:
-            state.momentum = torch.empty_like(like)
+            state.momentum = _state_buffer(like)
             row.flags |= _native.RF_ROWF_MOMENTUM_INIT
     row.momentum = _p(state.momentum)
     row.residual = _p(state.residual)

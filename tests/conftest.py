@@ -9,6 +9,11 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
         sys.path.insert(0, p)
 
 
+# the staged reference suite (tools/vendor_reference_suite.py) runs in its own subprocess
+# (tests/test_gpu_reference_suite.py), never collected with this repo's tests
+collect_ignore_glob = ["_refsuite/*"]
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running")

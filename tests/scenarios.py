@@ -134,13 +134,14 @@ def drive(api, spec):
     T, D, inputs = _inputs(spec)
     cfg = api.PipelineConfig(**dict(dict(frames=96, channels=8), **spec["config"]))
     pipe = api.StreamPipeline(cfg, request=_build_request(api, spec, inputs, T))
-    recs, ticks_ts = [], []
+    recs, ticks_ts, snaps = [], [], []
 
     def run(n):
         for _ in range(n):
             for rec in pipe.tick():
                 recs.append(rec)
             ticks_ts.append([(float(s), i) for s, i in pipe.last_timesteps])
+            snaps.append(snapshot_str(pipe.snapshot()))
 
     for op in spec["ops"]:
         kind = op[0]
@@ -164,12 +165,21 @@ def drive(api, spec):
                 run(1)
         else:
             raise ValueError(kind)
-    return _trace(recs, ticks_ts, pipe)
+    return _trace(recs, ticks_ts, pipe, snaps)
 
 
-def _trace(recs, ticks_ts, pipe):
+def snapshot_str(snap) -> str:
+    """Canonical text of a PipelineSnapshot (reference pipeline.py:221-244, 289-304): every
+    field, floats by repr, so equal strings mean equal snapshots."""
+    slots = ";".join("-" if v is None else f"{float(v.denoise)!r},{int(v.step)},{v.schedule_id}" for v in snap.slots)
+    vals = ",".join(repr(float(d)) for d in sorted(snap.denoise_values()))
+    return f"{snap.tick}|{snap.mode}|{float(snap.denoise)!r}|{snap.queue_depth}|{slots}|{vals}"
+
+
+def _trace(recs, ticks_ts, pipe, snaps):
     n = len(recs)
     out = {
+        "snapshot": np.array(snaps, dtype=object).astype(str),
         "tick": np.array([r.tick for r in recs], dtype=np.int64),
         "completion_index": np.array([r.completion_index for r in recs], dtype=np.int64),
         "submission_id": np.array([r.submission_id for r in recs], dtype=np.int64),
@@ -218,12 +228,13 @@ def drive_oracle(spec):
     pipe = O.Pipeline(depth=c["depth"], steps=c["steps"], frames=c["frames"], channels=c["channels"],
                       mode=c.get("mode", "per-slot"), seed=c.get("seed", 0), denoise=c.get("denoise", 1.0),
                       jitter=c.get("model_jitter", 0.1), request=req)
-    recs, ticks_ts = [], []
+    recs, ticks_ts, snaps = [], [], []
 
     def run(n):
         for _ in range(n):
             recs.extend(pipe.tick())
             ticks_ts.append([(float(s), i) for s, i in pipe.last_timesteps])
+            snaps.append(snapshot_str(pipe.snapshot()))
 
     for op in spec["ops"]:
         kind = op[0]
@@ -250,9 +261,9 @@ def drive_oracle(spec):
         tick_index = pipe.tick_index
         completions_total = pipe.completions
 
-    return _trace(recs, ticks_ts, _P)
+    return _trace(recs, ticks_ts, _P, snaps)
 
 
 # fields compared bit-exactly (integer / id / flag bookkeeping)
 EXACT_FIELDS = ("tick", "completion_index", "submission_id", "schedule_id", "denoise", "hybrid",
-                "decode_skipped", "ts_count", "ts_sigma", "ts_id", "final_tick", "completions_total")
+                "decode_skipped", "ts_count", "ts_sigma", "ts_id", "final_tick", "completions_total", "snapshot")

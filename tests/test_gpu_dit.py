@@ -27,16 +27,22 @@ def dit_mod():
     return dit
 
 
+@pytest.mark.parametrize("kernel", [0, 1])
 @pytest.mark.parametrize("B,Nq,Nk,H,Hk,grow", [(2, 750, 750, 16, 8, 0), (1, 100, 37, 4, 4, 0), (3, 750, 128, 16, 8, 0),
                                                (1, 128, 128, 2, 1, 0), (2, 300, 1000, 4, 2, 0),
-                                               (2, 256, 900, 4, 2, 1), (1, 200, 640, 2, 2, 1)])
-def test_tcgen05_attention_vs_sdpa(dit_mod, B, Nq, Nk, H, Hk, grow):
-    """grow: key norms rise along the sequence, so the running row max climbs tile after
-    tile (exercises the lazy O/l rescaling of the single-pass kernel)."""
+                                               (2, 256, 900, 4, 2, 1), (1, 200, 640, 2, 2, 1),
+                                               (2, 750, 750, 16, 8, 1), (1, 3000, 3000, 4, 2, 1)])
+def test_tcgen05_attention_vs_sdpa(dit_mod, kernel, B, Nq, Nk, H, Hk, grow):
+    """Every self-attention kernel (rf_attention_tc_bf16_kernel: 0 = the forward's default,
+    1 = 64-key tiles, one head per CTA) against SDPA.
+    grow: key norms rise along the sequence, so the running row max climbs tile after tile
+    (exercises the lazy O / l rescaling)."""
+    import ctypes
+
     from paper_2605_28657_b200 import _native
 
     lib = _native.load()
-    lib.rf_attention_tc_bf16.restype = int
+    lib.rf_attention_tc_bf16_kernel.restype = int
     g = torch.Generator(device="cuda").manual_seed(Nq * 11 + Nk)
     q = torch.randn(B * Nq, H * 128, device="cuda", generator=g).bfloat16()
     k = torch.randn(B * Nk, Hk * 128, device="cuda", generator=g)
@@ -48,16 +54,16 @@ def test_tcgen05_attention_vs_sdpa(dit_mod, B, Nq, Nk, H, Hk, grow):
     vt = torch.zeros(B, Hk, 128, nk_pad, device="cuda", dtype=torch.bfloat16)
     vt[..., :Nk] = v.reshape(B, Nk, Hk, 128).permute(0, 2, 3, 1)
     out = torch.empty(B * Nq, H * 128, device="cuda", dtype=torch.bfloat16)
-    vp = __import__("ctypes").c_void_p
-    _native.check(lib.rf_attention_tc_bf16(vp(q.data_ptr()), vp(k.data_ptr()), vp(vt.data_ptr()), vp(out.data_ptr()),
-                                           B, Nq, Nk, nk_pad, H, Hk, __import__("ctypes").c_int64(H * 128),
-                                           __import__("ctypes").c_int64(Hk * 128),
-                                           __import__("ctypes").c_int64(H * 128),
-                                           vp(torch.cuda.current_stream().cuda_stream)))
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    _native.check(lib.rf_attention_tc_bf16_kernel(kernel, vp(q.data_ptr()), vp(k.data_ptr()), vp(vt.data_ptr()),
+                                                  vp(out.data_ptr()), B, Nq, Nk, nk_pad, H, Hk, i64(H * 128),
+                                                  i64(Hk * 128), i64(H * 128),
+                                                  vp(torch.cuda.current_stream().cuda_stream)), "attention")
     qq = q.float().reshape(B, Nq, H, 128).transpose(1, 2)
     kk = k.float().reshape(B, Nk, Hk, 128).repeat_interleave(H // Hk, 2).transpose(1, 2)
     vv = v.float().reshape(B, Nk, Hk, 128).repeat_interleave(H // Hk, 2).transpose(1, 2)
     ref = torch.nn.functional.scaled_dot_product_attention(qq, kk, vv).transpose(1, 2).reshape(B * Nq, H * 128)
+    assert torch.isfinite(out).all()
     assert rel_rms(out, ref) < 1e-2
 
 
@@ -171,3 +177,44 @@ def test_full_size_pipeline_with_dit_is_reproducible(dit_mod):
     assert len(runs[0]) >= 8
     for a, b in zip(*runs):
         assert np.isfinite(a).all() and np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_stream_group_batches_rows_bit_identically(dit_mod, full):
+    """Two co-resident streams (different seeds, prompts, denoise schedules) ticked as a
+    StreamGroup -- one batched DiT forward over both rings' rows per tick -- emit exactly
+    the completions each stream emits when ticked alone (rows are independent)."""
+    import scenarios
+
+    import paper_2605_28657_b200 as rf
+
+    cfg = dit_mod.DiTConfig() if full else dit_mod.DiTConfig().small()
+    T, D = (1500, 64) if full else (96, 64)
+    dit = dit_mod.DiT(cfg, frames=T, max_rows=8)
+
+    def make(seed, vm):
+        src = scenarios.keyed(seed, "bench-source", (T, D))
+        req = rf.GenerationRequest(conditions=(rf.ConditionSet(rf.prompt_id(f"stream {seed}"), source=src),))
+        return rf.StreamPipeline(rf.PipelineConfig(depth=4, steps=8, frames=T, channels=D, seed=seed,
+                                                   denoise=1.0 if seed == 0 else 0.7),
+                                 request=req, velocity_model=vm)
+
+    ticks = 14
+    alone = []
+    for seed in (0, 1):
+        p = make(seed, dit_mod.DiTVelocity(dit))
+        recs = []
+        for _ in range(ticks):
+            recs += p.tick()
+        alone.append([(r.tick, r.submission_id, r.latent) for r in recs])
+        torch.cuda.synchronize()
+    shared = dit_mod.DiTVelocity(dit)
+    group = rf.StreamGroup([make(0, shared), make(1, shared)])
+    together = [[], []]
+    for _ in range(ticks):
+        for i, recs in enumerate(group.tick()):
+            together[i] += [(r.tick, r.submission_id, r.latent) for r in recs]
+    for a, b in zip(alone, together):
+        assert len(a) == len(b) >= 3
+        for (ta, sa, la), (tb, sb, lb) in zip(a, b):
+            assert ta == tb and sa == sb and np.array_equal(la, lb)
