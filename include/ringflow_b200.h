@@ -185,6 +185,23 @@ int rf_decode_window(const double *latent, int64_t frames, int64_t channels,
                      int64_t overlap, int32_t full, int16_t *out, void *workspace,
                      int64_t workspace_bytes, void *stream);
 
+/* The same decode on the tensor cores (csrc/rf_decode_tc.cu): the conv stack and the
+ * upsampler as implicit GEMMs (tcgen05 kind::f16, every operand split into two fp16
+ * pieces hi + lo, three MMAs per product, fp32 accumulation), quantize_pcm fused; within
+ * 1 LSB of the float64 reference, windowed == full bit for bit when overlap >= rf.
+ * Shapes: C <= 64, hop a multiple of 16, dilations <= 16, receptive field <= 56; anything
+ * else uses rf_decode_window.  rf_decode_tc_packed_bytes returns 0 for an unsupported
+ * shape.  rf_decode_tc_pack converts the float64 weights once (codec construction) into
+ * `packed` (device, 16-byte aligned); rf_decode_window_tc then reads only `packed`.
+ *   out: device int16 [(stop - start) * hop], 16-byte aligned. */
+int64_t rf_decode_tc_packed_bytes(int64_t channels, int64_t hop, int32_t n_layers);
+int rf_decode_tc_pack(const double *kernels, int32_t n_layers, int64_t channels,
+                      const double *upsample_t, int64_t hop, void *packed, int64_t packed_bytes,
+                      void *stream);
+int rf_decode_window_tc(const double *latent, int64_t frames, int64_t channels, const void *packed,
+                        const int32_t *dilations, int32_t n_layers, int64_t hop, int64_t start,
+                        int64_t stop, int64_t overlap, int32_t full, int16_t *out, void *stream);
+
 /* ToyCodec.encode (codec.py:168-174): latent[f, c] = sum_k samples[f*hop + k] * proj[c, k].
  *   samples: device float64 [frames * hop]; proj_t: device [hop, C] (the reference's
  *   encode_proj [C, hop], transposed); latent: device float64 [frames, C]. */

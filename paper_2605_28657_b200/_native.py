@@ -86,7 +86,8 @@ EXPORTS = (
     "rf_abi_version", "rf_last_error", "rf_device_sm_count",
     "rf_normal_workspace_bytes", "rf_normal_fill", "rf_uniform_fill",
     "rf_tick_solve", "rf_x0_compose", "rf_admit_init", "rf_emit_stats", "rf_reduce_workspace_elems",
-    "rf_decode_workspace_bytes", "rf_decode_window", "rf_encode_frames", "rf_mse", "rf_gemm_bf16",
+    "rf_decode_workspace_bytes", "rf_decode_window", "rf_decode_tc_packed_bytes", "rf_decode_tc_pack",
+    "rf_decode_window_tc", "rf_encode_frames", "rf_mse", "rf_gemm_bf16",
     "rf_dit_workspace_bytes", "rf_dit_create", "rf_dit_destroy", "rf_dit_forward",
     "rf_dit_output", "rf_attention_tc_bf16", "rf_attention_tc_bf16_kernel",
 )
@@ -152,6 +153,13 @@ def _declare(lib):
     lib.rf_decode_window.restype = i32
     lib.rf_decode_window.argtypes = [vp, i64, i64, vp, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
                                      vp, i64, i64, i64, i64, ctypes.c_int32, vp, vp, i64, vp]
+    lib.rf_decode_tc_packed_bytes.restype = i64
+    lib.rf_decode_tc_packed_bytes.argtypes = [i64, i64, i32]
+    lib.rf_decode_tc_pack.restype = i32
+    lib.rf_decode_tc_pack.argtypes = [vp, i32, i64, vp, i64, vp, i64, vp]
+    lib.rf_decode_window_tc.restype = i32
+    lib.rf_decode_window_tc.argtypes = [vp, i64, i64, vp, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+                                        i64, i64, i64, i64, ctypes.c_int32, vp, vp]
     lib.rf_encode_frames.restype = i32
     lib.rf_encode_frames.argtypes = [vp, i64, i64, vp, i64, vp, vp]
     lib.rf_gemm_bf16.restype = i32

@@ -115,3 +115,50 @@ def test_encode_vs_reference(rf):
         assert np.max(np.abs(lat - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
     with pytest.raises(ValueError):
         codec.encode(np.zeros(hop + 1))
+
+
+@pytest.mark.parametrize("C,hop,dil", [(8, 64, (1, 2, 4, 8)), (16, 48, (1, 2, 4, 8)), (32, 128, (3, 5)),
+                                       (48, 256, (1, 2, 4, 8, 16)), (64, 1920, (1, 2, 4, 8)), (64, 16, (1,))])
+def test_tensor_core_decode_shapes(rf, C, hop, dil):
+    """rf_decode_window_tc (fp16 hi/lo operands on tcgen05) vs the float64 oracle: within
+    1 LSB over full decodes and windows, windowed == full bit-exact at overlap >= RF, and
+    within 1 LSB of the float64 CUDA-core kernel."""
+    codec = rf.ToyCodec(channels=C, hop=hop, dilations=dil)
+    assert codec.tensor_cores
+    T = 300
+    lat = scenarios.keyed(11, f"tc-{C}-{hop}", (T, C)) * 0.8
+    full = codec.full_decode(lat).samples
+    ref = O.Codec(C, hop, dil)
+    assert lsb(full, ref.full(lat)) <= LSB_TOL
+    rfield = sum(dil)
+    for a, b in ((0, 7), (5, 150), (140, 300), (299, 300), (37, 38)):
+        w = codec.windowed_decode(lat, (a, b), rfield).samples
+        assert np.array_equal(w, full[a * hop:b * hop])
+        assert lsb(w, ref.window(lat, a, b, rfield)) <= LSB_TOL
+        w0 = codec.windowed_decode(lat, (a, b), 2).samples      # overlap < RF: reference semantics
+        assert lsb(w0, ref.window(lat, a, b, 2)) <= LSB_TOL
+    if C & (C - 1) == 0:                                       # shapes the float64 kernel takes
+        packed = codec._packed
+        codec._packed = None
+        f64 = codec.full_decode(lat).samples
+        codec._packed = packed
+        assert lsb(full, f64) <= LSB_TOL
+
+
+def test_non_tensor_core_shape_uses_float64_kernel(rf):
+    codec = rf.ToyCodec(channels=8, hop=10)
+    assert not codec.tensor_cores
+    lat = scenarios.keyed(12, "f64-shape", (40, 8))
+    full = codec.full_decode(lat).samples
+    assert lsb(full, O.Codec(8, 10).full(lat)) <= LSB_TOL
+    assert np.array_equal(codec.windowed_decode(lat, (10, 20), 15).samples, full[100:200])
+
+
+def test_tensor_core_decode_large_latent_values(rf):
+    """Latents 20x the pipeline's scale (|x| up to ~100): still within 1 LSB.  The fp32
+    accumulator's rounding grows with the pre-activation magnitude; measured on B200:
+    <= 1 LSB up to 1000x the pipeline's scale, 2 LSB at 5000x."""
+    codec = rf.ToyCodec(channels=64, hop=1920)
+    lat = scenarios.keyed(13, "big", (60, 64)) * 20.0
+    full = codec.full_decode(lat).samples
+    assert lsb(full, O.Codec(64, 1920).full(lat)) <= LSB_TOL
