@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import struct
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -24,6 +25,7 @@ __all__ = [
     "Latent",
     "Curve",
     "NoiseSource",
+    "NoiseCache",
     "ShapeMismatchError",
     "content_hash",
     "prompt_id",
@@ -196,6 +198,55 @@ def fill_normals(draws, status: torch.Tensor = None, stream: int = None) -> None
         flags = int(status.item())
         if flags & _native.RF_STATUS_NOISE_SHORT:
             raise _native.NativeError("normal fill ran out of stream positions")
+
+
+class NoiseCache:
+    """Device cache of keyed normal draws: philox key -> float64 buffer.
+
+    A draw is a pure function of its key, and the key derives from (seed, content key,
+    step, tag) only -- denoise and curves are not in it (reference pipeline.py:95-96,
+    latents.py:118-150) -- so a stream regenerating the same request draws the same S x 2 + 1
+    tensors every generation.  Entries are LRU within ``capacity_bytes``; an entry used in
+    the current tick (``stamp``) is never evicted, so every pointer handed to this tick's
+    kernels stays valid (all users run on the owning pipeline's stream, in order).
+    """
+
+    def __init__(self, capacity_bytes: int, numel: int, device):
+        self.capacity_bytes = int(capacity_bytes)
+        self.numel = int(numel)
+        self._dev = device
+        self._entries: OrderedDict = OrderedDict()   # key -> [tensor, stamp]
+        self.hits = 0
+        self.misses = 0
+
+    @property
+    def bytes(self) -> int:
+        return len(self._entries) * self.numel * 8
+
+    def lookup(self, key: int, stamp: int):
+        """(buffer, hit): the cached draw for ``key``, or a buffer to fill for it."""
+        ent = self._entries.get(key)
+        if ent is not None:
+            ent[1] = stamp
+            self._entries.move_to_end(key)
+            self.hits += 1
+            return ent[0], True
+        self.misses += 1
+        buf = None
+        nbytes = self.numel * 8
+        while self._entries and self.bytes + nbytes > self.capacity_bytes:
+            old_key, old = next(iter(self._entries.items()))
+            if old[1] >= stamp:          # in use this tick: keep it
+                break
+            del self._entries[old_key]
+            buf = old[0]                 # reuse the evicted buffer (same size)
+        if buf is None:
+            buf = torch.empty(self.numel, dtype=torch.float64, device=self._dev)
+        self._entries[key] = [buf, stamp]
+        return buf, False
+
+    def clear(self) -> None:
+        self._entries.clear()
 
 
 @dataclass(frozen=True)

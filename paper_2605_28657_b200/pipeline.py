@@ -30,7 +30,7 @@ import torch
 
 from . import _device, _native
 from ._native import RfAdmit, RfEmit, RfRow
-from .latents import NoiseSource, ShapeMismatchError, content_hash, fill_normals
+from .latents import NoiseCache, NoiseSource, ShapeMismatchError, content_hash, fill_normals
 from .model import UNCOND_PROMPT, ConditionSet, ModelWeights, ToyFlowModel
 from .schedule import ScheduleCache, ScheduleMismatchError, TimestepSchedule, migrate_schedule
 from .solver import (
@@ -267,7 +267,10 @@ class StreamPipeline:
     """submit() -> tick() -> CompletionRecord stream, computed on one CUDA stream."""
 
     def __init__(self, config: PipelineConfig, request: Optional[GenerationRequest] = None,
-                 velocity_model=None):
+                 velocity_model=None, noise_cache_bytes: int = 256 << 20):
+        """velocity_model: None (the reference's toy model, inside the fused solver) or a
+        ``DiTVelocity``.  noise_cache_bytes: device budget of the keyed-noise cache
+        (``NoiseCache``); 0 regenerates every draw every tick."""
         self.config = config
         self._dev = _device.device()
         self._stream = torch.cuda.Stream(self._dev)
@@ -283,6 +286,8 @@ class StreamPipeline:
             # the emit reduction's partials: this pipeline's own (never shared across streams)
             self._reduce_elems = int(_native.load().rf_reduce_workspace_elems(T * D))
             self._reduce_scratch = torch.empty(max(self._reduce_elems, 1), dtype=torch.float64, device=self._dev)
+        self.noise_cache = (NoiseCache(noise_cache_bytes, T * D, self._dev)
+                            if noise_cache_bytes > 0 else None)
         self._stats_host = torch.empty((2, max(config.depth, 1)), dtype=torch.float64).pin_memory()
         self._status_host = torch.empty(1, dtype=torch.int32).pin_memory()
         self.velocity_model = velocity_model   # None: the toy model inside the fused kernel
@@ -572,8 +577,7 @@ class StreamPipeline:
                         w = c.weight_device()
                         row.cond_w[j] = None if w is None else w.data_ptr()
                 if jitter != 0.0:
-                    draws.append((slot.rng.key(k, "model"), nbuf[0]))
-                    row.noise_model = nbuf[0].data_ptr()
+                    row.noise_model = self._noise_for(slot.rng.key(k, "model"), nbuf[0], draws).data_ptr()
                     row.jitter_t = jitter * t_curr
             if self.velocity_model is not None and self.weights.version > 0:
                 row.flags |= _native.RF_ROWF_STYLE_V   # set_model_weights on the DiT path
@@ -593,8 +597,7 @@ class StreamPipeline:
                         raise MissingSourceError("sde_denoise_curve < 1 requires source latents")
                 row.solver = _native.RF_SOLVER_SDE
                 row.source = None if src is None else src.data_ptr()
-                draws.append((slot.rng.key(k, "sde"), nbuf[1]))
-                row.noise_step = nbuf[1].data_ptr()
+                row.noise_step = self._noise_for(slot.rng.key(k, "sde"), nbuf[1], draws).data_ptr()
                 if refine:
                     row.x0_target = dev["x0_target"].data_ptr()
             else:
@@ -603,8 +606,7 @@ class StreamPipeline:
                     row.flags |= _native.RF_ROWF_ODE_MORPH
                     row.x0_target = dev["x0_target"].data_ptr()
                 if host["ode_noise_curve"] is not None:
-                    draws.append((slot.rng.key(k, "ode"), nbuf[1]))
-                    row.noise_step = nbuf[1].data_ptr()
+                    row.noise_step = self._noise_for(slot.rng.key(k, "ode"), nbuf[1], draws).data_ptr()
             if self.velocity_model is None:
                 rows.append(row)
         if draws:
@@ -625,6 +627,17 @@ class StreamPipeline:
         for slot in slots:
             slot.state.step += 1
             slot.schedule_ids_used.add(slot.schedule.schedule_id)
+
+    def _noise_for(self, key: int, fallback: torch.Tensor, draws: list) -> torch.Tensor:
+        """The device draw for ``key``: a noise-cache entry (queued for generation on a
+        miss) or, without the cache, ``fallback`` (always queued)."""
+        if self.noise_cache is None:
+            draws.append((key, fallback))
+            return fallback
+        buf, hit = self.noise_cache.lookup(key, self._tick_index)
+        if not hit:
+            draws.append((key, buf))
+        return buf
 
     def _noise_buffers(self, slot: _Slot):
         idx = slot._ring_index  # noqa: SLF001
@@ -735,8 +748,7 @@ class StreamPipeline:
             self._check_request(slot.request)
         draws, admits = [], (RfAdmit * len(slots))()
         for j, slot in enumerate(slots):
-            nbuf = self._noise_buffers(slot)[2]
-            draws.append((slot.rng.key(0, "init"), nbuf))
+            nbuf = self._noise_for(slot.rng.key(0, "init"), self._noise_buffers(slot)[2], draws)
             admits[j].x = slot.x.data_ptr()
             admits[j].noise = nbuf.data_ptr()
             if slot.denoise < 1.0:
@@ -746,12 +758,13 @@ class StreamPipeline:
                 admits[j].source = None
                 admits[j].denoise = 1.0
         ev = self._phase_begin("admit")
-        fill_normals(draws, self._status, self._stream.cuda_stream)
+        if draws:
+            fill_normals(draws, self._status, self._stream.cuda_stream)
         lib = _native.load()
         _native.check(lib.rf_admit_init(admits, len(slots), slots[0].x.numel(), self._stream.cuda_stream),
                       "rf_admit_init")
         self._phase_end("admit", ev)
-        self.launches_last_tick += 3
+        self.launches_last_tick += 3 if draws else 1
 
     # ----------------------------------------------------- sequential renderer
     def render(self, request: Optional[GenerationRequest] = None, denoise: Optional[float] = None):

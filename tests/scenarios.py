@@ -133,7 +133,8 @@ def drive(api, spec):
     """Run a scenario through a ringflow-API module; returns flat trace arrays."""
     T, D, inputs = _inputs(spec)
     cfg = api.PipelineConfig(**dict(dict(frames=96, channels=8), **spec["config"]))
-    pipe = api.StreamPipeline(cfg, request=_build_request(api, spec, inputs, T))
+    kw = {"noise_cache_bytes": spec["noise_cache_bytes"]} if "noise_cache_bytes" in spec else {}
+    pipe = api.StreamPipeline(cfg, request=_build_request(api, spec, inputs, T), **kw)
     recs, ticks_ts, snaps = [], [], []
 
     def run(n):

@@ -51,6 +51,36 @@ def test_scenario_matches_reference(rf, goldens, name):
     assert np.array_equal(r_gpu[ok] == 0.0, r_ref[ok] == 0.0)
 
 
+@pytest.mark.parametrize("name", ["migration", "multi_cond", "per_frame_blend", "weight_swap", "ode_curves", "guidance_self_apg"])
+@pytest.mark.parametrize("cache_entries", [0, 1, 3])
+def test_noise_cache_sizes_bit_exact(rf, goldens, name, cache_entries):
+    """The keyed-noise cache changes no byte: disabled (every draw
+    regenerated), and budgets below one tick's draws (constant eviction, in-tick entries
+    protected) give the reference's traces exactly."""
+    spec = dict(scenarios.SPECS[name])
+    numel = spec["config"].get("frames", 96) * spec["config"].get("channels", 8)
+    spec["noise_cache_bytes"] = cache_entries * numel * 8
+    tr = scenarios.drive(rf, spec)
+    for k in scenarios.EXACT_FIELDS:
+        assert np.array_equal(tr[k], goldens[f"sc_{name}_{k}"]), k
+    assert np.array_equal(np.array([sha(x) for x in tr["latents"]]), goldens[f"sc_{name}_latent_sha"])
+
+
+def test_noise_cache_steady_state_hits(rf):
+    """Steady state with a held request: after the first generation every draw hits."""
+    cfg = rf.PipelineConfig(depth=4, steps=8, frames=250, channels=8)
+    src = scenarios.keyed(3, "cache-src", (250, 8))
+    pipe = rf.StreamPipeline(cfg, request=rf.GenerationRequest(
+        conditions=(rf.ConditionSet(prompt_hash=rf.content_hash("p"), source=src),)))
+    for _ in range(20):
+        pipe.tick()
+    h0, m0 = pipe.noise_cache.hits, pipe.noise_cache.misses
+    assert m0 == 17            # S x (model, sde) + the admission draw, once
+    for _ in range(16):
+        pipe.tick()
+    assert pipe.noise_cache.misses == m0 and pipe.noise_cache.hits > h0
+
+
 def _c2_spec(depth, steps, ticks, frames=1500, channels=64, extra_ops=(), **req):
     return dict(config=dict(depth=depth, steps=steps, frames=frames, channels=channels),
                 request=dict(prompt="bench prompt", source="src", **req), ops=[("tick", ticks), *extra_ops])
@@ -89,11 +119,13 @@ def test_stream_equals_render(rf):
     assert np.array_equal(steady, pipe.render(req))
 
 
-def test_launch_count_and_no_sync_without_emit(rf):
+@pytest.mark.parametrize("cache", [True, False])
+def test_launch_count_and_no_sync_without_emit(rf, cache):
     T, D = 1500, 64
     src = scenarios.keyed(100, "source", (T, D))
     req = rf.GenerationRequest(conditions=(rf.ConditionSet(rf.prompt_id("p"), source=src),))
-    pipe = rf.StreamPipeline(rf.PipelineConfig(depth=4, steps=8, frames=T, channels=D), request=req)
+    pipe = rf.StreamPipeline(rf.PipelineConfig(depth=4, steps=8, frames=T, channels=D), request=req,
+                             noise_cache_bytes=(256 << 20) if cache else 0)
     for _ in range(40):
         pipe.tick()
     counts = []
@@ -103,7 +135,10 @@ def test_launch_count_and_no_sync_without_emit(rf):
     # steady state at depth 4, S=8: a completion every 2 ticks
     assert sorted(c for c, _ in counts) == [0, 0, 1, 1]
     for n_emit, launches in counts:
-        assert launches == (3 + (2 + 3 if n_emit else 0))
+        if cache:   # every draw hits: solve (+ emit statistics + admission init)
+            assert launches == 1 + (2 + 1 if n_emit else 0)
+        else:       # noise (2) + solve (+ emit (2) + admission noise (2) + init)
+            assert launches == 3 + (2 + 3 if n_emit else 0)
 
 
 def test_backpressure_and_errors(rf):
