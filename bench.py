@@ -494,7 +494,28 @@ def run_ours(args):
         # visible part of the timed region
         t_phase = timed_ticks(tp, 16, flush, tp.stream, phases=True)[3]
         sb = DEPTH * solve_bytes_per_row(True)
+        # host-inclusive rate: ticks back to back (no flush), wall clock
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        w_done = sum(len(tp.tick()) for _ in range(256))
+        torch.cuda.synchronize()
+        w_s = time.perf_counter() - w0
+        nc = tp.noise_cache
+        cache_stats = {"hits": nc.hits, "misses": nc.misses, "resident_bytes": nc.bytes}
+        del tp
+        # the same leg with the noise cache off (every draw regenerated every tick)
+        tq = rf.StreamPipeline(conf, request=make_request(rf, rank), noise_cache_bytes=0)
+        for _ in range(32):
+            tq.tick()
+        torch.cuda.synchronize()
+        q_ms, q_done, _ = timed_ticks(tq, 64, flush, tq.stream)
+        del tq
         toy = {"value": round(t_done / (t_ms * 1e-3), 2), "unit": UNIT, "ms_per_step": round(t_ms / 64, 5),
+               "wall": {"value": round(w_done / w_s, 1), "unit": UNIT, "us_per_tick": round(w_s / 256 * 1e6, 1),
+                        "note": "256 ticks back to back, wall clock (host Python + device), no L2 flush"},
+               "noise_cache": dict(cache_stats, note="device cache of keyed draws (seed, content key, step, tag); "
+                                   "steady state regenerates nothing"),
+               "noise_cache_off": {"value": round(q_done / (q_ms * 1e-3), 2), "ms_per_step": round(q_ms / 64, 5)},
                "phase_ms": {k: round(v, 5) for k, v in t_phase.items()},
                "solver_roofline": {"bound": "hbm", "kernel": "rf_tick_kernel",
                                    "achieved": round(sb / (t_phase["solve"] * 1e-3) / 1e9, 1), "peak": hbm_peak,

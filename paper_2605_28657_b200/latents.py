@@ -215,7 +215,7 @@ class NoiseCache:
         self.capacity_bytes = int(capacity_bytes)
         self.numel = int(numel)
         self._dev = device
-        self._entries: OrderedDict = OrderedDict()   # key -> [tensor, stamp]
+        self._entries: OrderedDict = OrderedDict()   # key -> [tensor, stamp, filled]
         self.hits = 0
         self.misses = 0
 
@@ -224,13 +224,17 @@ class NoiseCache:
         return len(self._entries) * self.numel * 8
 
     def lookup(self, key: int, stamp: int):
-        """(buffer, hit): the cached draw for ``key``, or a buffer to fill for it."""
+        """(buffer, hit): the cached draw for ``key``, or a buffer to fill for it (then
+        ``filled`` once its fill is queued; an entry never filled stays a miss)."""
         ent = self._entries.get(key)
         if ent is not None:
             ent[1] = stamp
             self._entries.move_to_end(key)
-            self.hits += 1
-            return ent[0], True
+            if ent[2]:
+                self.hits += 1
+                return ent[0], True
+            self.misses += 1
+            return ent[0], False
         self.misses += 1
         buf = None
         nbytes = self.numel * 8
@@ -242,8 +246,15 @@ class NoiseCache:
             buf = old[0]                 # reuse the evicted buffer (same size)
         if buf is None:
             buf = torch.empty(self.numel, dtype=torch.float64, device=self._dev)
-        self._entries[key] = [buf, stamp]
+        self._entries[key] = [buf, stamp, False]
         return buf, False
+
+    def filled(self, keys) -> None:
+        """Mark entries whose generation has been queued on the owning stream."""
+        for key in keys:
+            ent = self._entries.get(key)
+            if ent is not None:
+                ent[2] = True
 
     def clear(self) -> None:
         self._entries.clear()

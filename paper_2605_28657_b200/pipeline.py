@@ -216,7 +216,7 @@ class SharedRegistry:
 
 class _Slot:
     __slots__ = ("submission_id", "request", "denoise", "schedule", "x", "state", "rng",
-                 "admitted_tick", "schedule_ids_used", "migrated", "_ring_index")
+                 "admitted_tick", "schedule_ids_used", "migrated", "_ring_index", "_row_tpl")
 
     def __init__(self, submission_id, request, denoise, schedule, x, state, rng, admitted_tick):
         self.submission_id = submission_id
@@ -230,6 +230,7 @@ class _Slot:
         self.schedule_ids_used = {schedule.schedule_id}
         self.migrated = False
         self._ring_index = None
+        self._row_tpl = None            # (key, RfRow): the row's per-generation fields
 
     @property
     def step(self) -> int:
@@ -281,15 +282,23 @@ class StreamPipeline:
             self._ring = torch.zeros((config.depth, T, D), dtype=torch.float64, device=self._dev)
             # per slot: [0] model noise, [1] step noise (sde/ode), [2] admission noise
             self._noise = torch.empty((config.depth, 3, T, D), dtype=torch.float64, device=self._dev)
-            self._status = torch.zeros(1, dtype=torch.int32, device=self._dev)
-            self._stats = torch.empty((2, max(config.depth, 1)), dtype=torch.float64, device=self._dev)
+            # per-slot views made once (tensor indexing costs microseconds of host time per tick)
+            self._noise_views = [[self._noise[i, j] for j in range(3)] for i in range(config.depth)]
+            # emit statistics [2, depth] and the status word share one buffer (one read-back)
+            nd = max(config.depth, 1)
+            self._emitbuf = torch.zeros(2 * nd + 1, dtype=torch.float64, device=self._dev)
+            self._stats = self._emitbuf[:2 * nd].view(2, nd)
+            self._status = self._emitbuf[2 * nd:].view(torch.int32)[:1]
+            self._stats_ptrs = (self._stats[0].data_ptr(), self._stats[1].data_ptr())
             # the emit reduction's partials: this pipeline's own (never shared across streams)
             self._reduce_elems = int(_native.load().rf_reduce_workspace_elems(T * D))
             self._reduce_scratch = torch.empty(max(self._reduce_elems, 1), dtype=torch.float64, device=self._dev)
         self.noise_cache = (NoiseCache(noise_cache_bytes, T * D, self._dev)
                             if noise_cache_bytes > 0 else None)
-        self._stats_host = torch.empty((2, max(config.depth, 1)), dtype=torch.float64).pin_memory()
-        self._status_host = torch.empty(1, dtype=torch.int32).pin_memory()
+        self._emitbuf_host = torch.zeros(2 * nd + 1, dtype=torch.float64).pin_memory()
+        self._stats_host = self._emitbuf_host[:2 * nd].view(2, nd)
+        self._status_host = self._emitbuf_host[2 * nd:].view(torch.int32)[:1]
+        self._emit_event = torch.cuda.Event()
         self.velocity_model = velocity_model   # None: the toy model inside the fused kernel
         self.cache = ScheduleCache()
         self.registry = SharedRegistry(T, D)
@@ -313,6 +322,8 @@ class StreamPipeline:
         self.launches_last_tick = 0
         self.rows_last_tick = 0
         self._phases = None  # {phase: [(start_event, end_event), ...]} when timing is on
+        self._views: dict = {}            # id(request) -> cached curve view (see _curve_view)
+        self._views_version = -1
 
     # ------------------------------------------------------------- profiling
     def enable_phase_timing(self, on: bool = True) -> dict:
@@ -377,13 +388,13 @@ class StreamPipeline:
             return self._tick_index
 
     def set_shared_curve(self, name: str, value) -> int:
-        with self._lock, torch.cuda.stream(self._stream):
+        with self._lock, _device.on_stream(self._stream):
             self._mark_reference()
             self.registry.set(name, value)
             return self._tick_index
 
     def set_model_weights(self, offset) -> int:
-        with self._lock, torch.cuda.stream(self._stream):
+        with self._lock, _device.on_stream(self._stream):
             self._mark_reference()
             self.weights.swap_offset(offset)
             return self._tick_index
@@ -454,7 +465,7 @@ class StreamPipeline:
     # ------------------------------------------------------------------- tick
     def tick(self) -> list:
         """Advance every in-flight slot one step; emit finished latents (pipeline.py:372-398)."""
-        with self._lock, torch.cuda.stream(self._stream):
+        with self._lock, _device.on_stream(self._stream):
             active = self._tick_begin()
             if active:
                 self._step_slots(active)
@@ -503,7 +514,27 @@ class StreamPipeline:
             slot.migrated = True
 
     def _curve_view(self, slot: _Slot):
-        """Effective curves of a slot this step (pipeline.py:415-422): host + device views."""
+        """Effective curves of a slot this step (pipeline.py:415-422): (host dict, device
+        dict, the request's CurveSet, the solver's curve-pointer array).  A view depends
+        only on the request and the registry's contents, so it is built once per (request,
+        registry write) and reused by every slot and tick until the next registry write."""
+        req = slot.request
+        version = self.registry.write_count
+        if self._views_version != version:
+            self._views.clear()
+            self._views_version = version
+        view = self._views.get(id(req))
+        if view is None or view[0] is not req:
+            host, dev, base = self._build_curve_view(slot)
+            ptrs = (_native.c_dptr * _native.RF_NUM_CURVES)()
+            for name, idx in _native.CURVE_INDEX.items():
+                t = dev[name]
+                ptrs[idx] = None if t is None else t.data_ptr()
+            view = (req, host, dev, base, ptrs)
+            self._views[id(req)] = view
+        return view[1], view[2], view[3], view[4]
+
+    def _build_curve_view(self, slot: _Slot):
         base = slot.request.curves
         reg_host = self.registry.overlay()
         reg_dev = self.registry.device_overlay()
@@ -560,48 +591,28 @@ class StreamPipeline:
             k = slot.step
             t_curr = float(slot.schedule.sigmas[k])
             t_next = float(slot.schedule.sigmas[k + 1])
-            host, dev, base = self._curve_view(slot)
+            host, dev, base, curve_ptrs = self._curve_view(slot)
             req = slot.request
             nbuf = self._noise_buffers(slot)
-            row = RfRow() if self.velocity_model is None else rows[i]
-            row.x = slot.x.data_ptr()
-            row.t_curr, row.t_next = t_curr, t_next
-            conds = req.conditions
             if self.velocity_model is None:
-                row.n_cond = len(conds)
-                if row.n_cond > _native.RF_MAX_COND:
-                    raise NotImplementedError(f"at most {_native.RF_MAX_COND} conditions per request")
-                for j, c in enumerate(conds):
-                    row.cond_x0[j] = self.model.x0_partial(c).data_ptr()
-                    if len(conds) > 1:
-                        w = c.weight_device()
-                        row.cond_w[j] = None if w is None else w.data_ptr()
+                row = _native.RfRow.from_buffer_copy(self._row_template(slot, host, base, curve_ptrs))
                 if jitter != 0.0:
                     row.noise_model = self._noise_for(slot.rng.key(k, "model"), nbuf[0], draws).data_ptr()
                     row.jitter_t = jitter * t_curr
-            if self.velocity_model is not None and self.weights.version > 0:
-                row.flags |= _native.RF_ROWF_STYLE_V   # set_model_weights on the DiT path
-            curve_pointers(row, lambda n: dev[n])
+            else:
+                row = rows[i]
+                self._row_static(row, slot, host, base, curve_ptrs)
+            row.t_curr, row.t_next = t_curr, t_next
             if base.guidance_enabled:
                 neg_kind, flags = guidance_plan(base.rcfg_mode, slot.state, True)
                 row.neg_kind, row.flags = neg_kind, row.flags | flags
-                if neg_kind == _native.RF_NEG_UNCOND and self.velocity_model is None:
-                    row.uncond_x0 = self.model.x0_partial(_UNCOND).data_ptr()
                 prepare_guidance_state(row, slot.state, host["apg_momentum"] is not None, slot.x)
             refine = host["x0_target"] is not None and slot.state.in_refinement_half()
             if req.solver == "sde":
-                src = conds[0].source_device()
-                if src is None:
-                    curve = host["sde_denoise_curve"]
-                    if curve is not None and np.any(curve < 1.0):
-                        raise MissingSourceError("sde_denoise_curve < 1 requires source latents")
-                row.solver = _native.RF_SOLVER_SDE
-                row.source = None if src is None else src.data_ptr()
                 row.noise_step = self._noise_for(slot.rng.key(k, "sde"), nbuf[1], draws).data_ptr()
                 if refine:
                     row.x0_target = dev["x0_target"].data_ptr()
             else:
-                row.solver = _native.RF_SOLVER_ODE
                 if refine:
                     row.flags |= _native.RF_ROWF_ODE_MORPH
                     row.x0_target = dev["x0_target"].data_ptr()
@@ -612,6 +623,8 @@ class StreamPipeline:
         if draws:
             ev = self._phase_begin("noise")
             fill_normals(draws, self._status, self._stream.cuda_stream)
+            if self.noise_cache is not None:
+                self.noise_cache.filled(key for key, _ in draws)
             self._phase_end("noise", ev)
             self.launches_last_tick += 2
         lib = _native.load()
@@ -639,11 +652,53 @@ class StreamPipeline:
             draws.append((key, buf))
         return buf
 
+    def _row_static(self, row, slot: _Slot, host: dict, base, curve_ptrs) -> None:
+        """Row fields fixed for a slot's generation (until a registry / weights write):
+        latent, conditions, curves, solver and source (reference pipeline.py:424-464)."""
+        req = slot.request
+        row.x = slot.x.data_ptr()
+        if self.velocity_model is None:
+            conds = req.conditions
+            row.n_cond = len(conds)
+            if row.n_cond > _native.RF_MAX_COND:
+                raise NotImplementedError(f"at most {_native.RF_MAX_COND} conditions per request")
+            for j, c in enumerate(conds):
+                row.cond_x0[j] = self.model.x0_partial(c).data_ptr()
+                if len(conds) > 1:
+                    w = c.weight_device()
+                    row.cond_w[j] = None if w is None else w.data_ptr()
+            if base.guidance_enabled:
+                row.uncond_x0 = self.model.x0_partial(_UNCOND).data_ptr()
+        elif self.weights.version > 0:
+            row.flags |= _native.RF_ROWF_STYLE_V   # set_model_weights on the DiT path
+        row.curves = curve_ptrs
+        if req.solver == "sde":
+            src = req.conditions[0].source_device()
+            if src is None:
+                curve = host["sde_denoise_curve"]
+                if curve is not None and np.any(curve < 1.0):
+                    raise MissingSourceError("sde_denoise_curve < 1 requires source latents")
+            row.solver = _native.RF_SOLVER_SDE
+            row.source = None if src is None else src.data_ptr()
+        else:
+            row.solver = _native.RF_SOLVER_ODE
+
+    def _row_template(self, slot: _Slot, host: dict, base, curve_ptrs):
+        """The toy-path row's static fields, built once per (slot, registry write, weights
+        write) and copied per tick."""
+        key = (self._views_version, self.weights.version)
+        tpl = slot._row_tpl  # noqa: SLF001
+        if tpl is None or tpl[0] != key:
+            row = _native.RfRow()
+            self._row_static(row, slot, host, base, curve_ptrs)
+            tpl = slot._row_tpl = (key, row)  # noqa: SLF001
+        return tpl[1]
+
     def _noise_buffers(self, slot: _Slot):
         idx = slot._ring_index  # noqa: SLF001
         if idx is None:  # render(): private buffers
-            return slot.x.new_empty((3,) + tuple(slot.x.shape))
-        return self._noise[idx]
+            return list(slot.x.new_empty((3,) + tuple(slot.x.shape)))
+        return self._noise_views[idx]
 
     def _emit(self, finished: list) -> list:
         """_emit for every finished slot, in slot-index order (pipeline.py:466-491)."""
@@ -667,15 +722,14 @@ class StreamPipeline:
         ev = self._phase_begin("emit")
         _native.check(lib.rf_emit_stats(
             emits, n, slot.x.numel(), None if last is None else last.data_ptr(),
-            None if ref is None else ref.data_ptr(), self._stats[0].data_ptr(),
-            self._stats[1].data_ptr(), self._status.data_ptr(), self._reduce_scratch.data_ptr(),
+            None if ref is None else ref.data_ptr(), self._stats_ptrs[0],
+            self._stats_ptrs[1], self._status.data_ptr(), self._reduce_scratch.data_ptr(),
             self._reduce_elems, self._stream.cuda_stream),
             "rf_emit_stats")
         self._phase_end("emit", ev)
         self.launches_last_tick += 2
-        self._stats_host.copy_(self._stats, non_blocking=True)
-        self._status_host.copy_(self._status, non_blocking=True)
-        done = torch.cuda.Event()
+        self._emitbuf_host.copy_(self._emitbuf, non_blocking=True)
+        done = self._emit_event
         done.record(self._stream)
         return recs_dev, done
 
@@ -760,6 +814,8 @@ class StreamPipeline:
         ev = self._phase_begin("admit")
         if draws:
             fill_normals(draws, self._status, self._stream.cuda_stream)
+            if self.noise_cache is not None:
+                self.noise_cache.filled(key for key, _ in draws)
         lib = _native.load()
         _native.check(lib.rf_admit_init(admits, len(slots), slots[0].x.numel(), self._stream.cuda_stream),
                       "rf_admit_init")
@@ -769,7 +825,7 @@ class StreamPipeline:
     # ----------------------------------------------------- sequential renderer
     def render(self, request: Optional[GenerationRequest] = None, denoise: Optional[float] = None):
         """Batch-mode oracle through the same step code (pipeline.py:546-566)."""
-        with self._lock, torch.cuda.stream(self._stream):
+        with self._lock, _device.on_stream(self._stream):
             request = request if request is not None else self._template
             if request is None:
                 raise ValueError("no request given and no template set")
