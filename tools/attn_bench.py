@@ -1,6 +1,7 @@
 """Self-attention kernels at BASELINE config-2 shape (4 rows x 750 tokens, 16 / 8 heads of 128):
-standalone time (CUDA events, warm, median of 50) and rel-RMS vs SDPA, per kernel choice of
-rf_attention_tc_bf16_kernel.  python tools/attn_bench.py [B N]"""
+device time (20 launches per CUDA graph replay, median of 10) and rel-RMS vs SDPA of the
+self-attention kernel (rf_attention_tc_bf16_kernel).
+python tools/attn_bench.py [B N]"""
 import ctypes
 import os
 import sys
@@ -38,18 +39,31 @@ def run(kern):
                                                   i64(Hk * 128), i64(H * 128), vp(st)), "attn")
 
 
-for kern, name in ((1, "fa64 (64-key, round 1)"), (0, "default")):
-    for _ in range(5):
+print(f"B={B} N={N}")
+for kern, name in ((0, "fa64 (default)"),):
+    for _ in range(3):
         run(kern)
     torch.cuda.synchronize()
+    # device time: 20 launches captured in a CUDA graph (the per-call host planning -- tensor
+    # maps, split rule -- is slower than the kernel, so eager launches would time the host)
+    gs = torch.cuda.Stream()
+    gs.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(gs):
+        st = gs.cuda_stream
+        run(kern)
+        with torch.cuda.graph(graph, stream=gs):
+            for _ in range(20):
+                run(kern)
+    torch.cuda.synchronize()
     ts = []
-    for _ in range(50):
+    for _ in range(10):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        run(kern)
+        graph.replay()
         b.record()
         ts.append((a, b))
     torch.cuda.synchronize()
-    us = sorted(x.elapsed_time(y) for x, y in ts)[25] * 1e3
+    us = sorted(x.elapsed_time(y) for x, y in ts)[5] * 1e3 / 20
     err = ((out.float() - ref).pow(2).mean().sqrt() / ref.pow(2).mean().sqrt()).item()
     print(f"{name:26s} {us:8.2f} us  {flops / us / 1e6:8.1f} TF/s  rel-rms {err:.2e}", flush=True)
