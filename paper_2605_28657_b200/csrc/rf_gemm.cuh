@@ -226,6 +226,9 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
 
     if (warp == 0) {
         if (elect_one()) {
+            // weights (B) stream through L2 once per forward: evict them first, so the
+            // activations the next kernels read stay resident
+            const uint64_t pol_w = createpolicy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
             int it = 0, t, kb0, kb1;
@@ -239,11 +242,11 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
                         const uint32_t fb = mapa_shared(&full[stage], 0);
                         tma_load_2d_pair(sA + stage * C::A_BYTES, &tma_a, fb, kb * BK, m0);
-                        tma_load_2d_pair(sB + stage * C::B_BYTES, &tma_b, fb, kb * BK, n0);
+                        tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tma_b, fb, kb * BK, n0, pol_w);
                     } else {
                         mbar_expect_tx(&full[stage], C::STAGE_BYTES);
                         tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * BK, m0);
-                        tma_load_2d(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0);
+                        tma_load_2d_hint(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0, pol_w);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
