@@ -69,7 +69,15 @@ struct Args {
     int cw, nch;              // chunk width, chunks per frame
     int slices;               // column slices per tile (grid = tiles x slices)
     int16_t *out;             // [nout * hop]
+    unsigned long long *trace;   // debugging: globaltimer stamps [cta][32] (null in production)
 };
+__device__ __forceinline__ void dtrace(const Args &A, int slot) {
+    if (A.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        A.trace[blockIdx.x * 32 + slot] = t;
+    }
+}
 
 __host__ __device__ constexpr uint32_t conv_bytes(int CP) { return 3u * 2u * CP * CP * 2u; }
 __host__ __device__ constexpr uint32_t chunk_bytes(int CP, int cw) { return 2u * CP * cw * 2u; }
@@ -153,17 +161,38 @@ __device__ __forceinline__ uint32_t quantize2(float x0, float x1) {
     asm("cvt.rzi.sat.s16.f32 %0, %1;" : "=h"(q1) : "f"(t1));
     return (uint32_t)(uint16_t)q0 | ((uint32_t)(uint16_t)q1 << 16);
 }
-// tanh(x) = 1 - 2 / (e^{2x} + 1) with one MUFU op (ex2) and the reciprocal by Newton
-// steps on the FMA pipe (the MUFU unit, 16 / clk / SM, bounds this epilogue otherwise):
-// absolute error ~1e-7, which is what reaches the output (the next operand keeps 22 bits)
-__device__ __forceinline__ float tanh_abs(float x) {
-    x = fminf(fmaxf(x, -9.f), 9.f);                     // tanh(9) = 1 - 3e-8
-    const float d = __expf(2.f * x) + 1.f;              // [1, 6.6e7]
-    float r = __uint_as_float(0x7EF311C3u - __float_as_uint(d));   // 1/d within 12.5%
-    r = r * (2.f - d * r);
-    r = r * (2.f - d * r);
-    r = r * (2.f - d * r);                              // 2^-24 relative
-    return 1.f - 2.f * r;
+// tanh(x) = 1 - 2 / (e^{2x} + 1) with one MUFU op (ex2) and the reciprocal by Newton steps
+// on the FMA pipe (the MUFU unit, 16 / clk / SM, would bound this epilogue otherwise):
+// absolute error ~1e-7, which is what reaches the output (the next operand keeps 22 bits).
+// Two values at a time on the packed fp32 pipe (FFMA2 / FMUL2, sm_100): the conv epilogue
+// is issue-bound, and the pair form halves its FMA-pipe instructions (1.45 -> 1.1 us per
+// layer of the 3-s window decode, tools/decode_trace.py).
+__device__ __forceinline__ uint64_t pack_f2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 unpack_f2(uint64_t r) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return make_float2(a, b);
+}
+__device__ __forceinline__ float2 tanh_abs2(float x0, float x1) {
+    x0 = fminf(fmaxf(x0, -9.f), 9.f);
+    x1 = fminf(fmaxf(x1, -9.f), 9.f);
+    const float d0 = __expf(2.f * x0) + 1.f, d1 = __expf(2.f * x1) + 1.f;
+    uint64_t d = pack_f2(d0, d1), r = pack_f2(__uint_as_float(0x7EF311C3u - __float_as_uint(d0)),
+                                              __uint_as_float(0x7EF311C3u - __float_as_uint(d1)));
+    const uint64_t two = pack_f2(2.f, 2.f);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {   // r = r * (2 - d * r)
+        uint64_t t;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(d ^ 0x8000000080000000ull), "l"(r), "l"(two));
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(r), "l"(t));
+    }
+    uint64_t y;   // 1 - 2 r
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(r), "l"(pack_f2(-2.f, -2.f)), "l"(pack_f2(1.f, 1.f)));
+    return unpack_f2(y);
 }
 
 template <int CP>
@@ -200,17 +229,19 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
             mbar_init(&ufull[i], 1);
-            mbar_init(&tmem_empty[i], kEpiWarps * 32);
+            mbar_init(&tmem_empty[i], kEpiWarps);   // one arrival per epilogue warp
         }
-        mbar_init(act_ready, kEpiWarps * 32);
+        mbar_init(act_ready, kEpiWarps);
         mbar_init(conv_full, 1);
         mbar_fence_init();
     }
+    if (threadIdx.x == 0) dtrace(A, 0);
     if (warp == kEpiWarps + 1) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) dtrace(A, 1);
 
     if (warp == kEpiWarps) {
         // ---------------------------------------------------------- weight producer
@@ -236,7 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
             for (int l = 0; l < A.L; ++l, ++blk) {
                 const int slot = blk & 1, use = blk >> 1;
                 mbar_wait(act_ready, l & 1);
+                dtrace(A, 2 + 2 * l);          // operand of layer l ready
                 mbar_wait(&full[slot], use & 1);
+                dtrace(A, 3 + 2 * l);          // weights of layer l ready
                 tc_fence_after();
                 const uint32_t w = sbase + S::RING + slot * S::SLOT;
                 const uint32_t idesc = idesc_f16(kRows, CP);
@@ -263,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
             }
             // upsampler chunks
             mbar_wait(act_ready, A.L & 1);
+            dtrace(A, 12);
             tc_fence_after();
             const uint32_t lbo_u = (uint32_t)A.cw * 16u;
             for (int c = c_begin; c < c_end; ++c, ++blk) {
@@ -271,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
                 const int n = (int)(A.hop - (int64_t)c * A.cw < A.cw ? A.hop - (int64_t)c * A.cw : A.cw);
                 mbar_wait(&tmem_empty[buf], (ub & 1) ^ 1);
                 mbar_wait(&full[slot], use & 1);
+                if (j < 4) dtrace(A, 13 + j);   // chunk weights ready
                 tc_fence_after();
                 const uint32_t u_hi = sbase + S::RING + slot * S::SLOT;
                 const uint32_t u_lo = u_hi + (uint32_t)CP * A.cw * 2u;
@@ -341,9 +376,11 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
             __half xh[8], xl[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const double v = fmin(fmax(x[it][e], -65504.0), 65504.0);
-                xh[e] = __double2half(v);
-                xl[e] = __double2half(v - (double)__half2float(xh[e]));
+                // one fp64 -> fp32 conversion, then the hi / lo split in fp32 (exact: f - hi
+                // is representable), as the activations are split -- fp64 ops are the slow ones
+                const float f = fminf(fmaxf((float)x[it][e], -65504.f), 65504.f);
+                xh[e] = __float2half_rn(f);
+                xl[e] = __float2half_rn(f - __half2float(xh[e]));
             }
             uint32_t h[4], lw[4];
 #pragma unroll
@@ -355,11 +392,14 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
             st_shared_v4(act_lo + kc * LBO_A + (kPad + r) * 16, make_uint4(lw[0], lw[1], lw[2], lw[3]));
         }
         fence_proxy_async_smem();
-        mbar_arrive(act_ready);
+        if (threadIdx.x == 0) dtrace(A, 17);   // latent operand written (thread 0's part)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(act_ready);   // per warp: 16 arrivals, not 512
         // conv layers: tanh, mask, split into the next operand (in place)
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         for (int l = 0; l < A.L; ++l) {
             mbar_wait(conv_full, l & 1);
+            if (threadIdx.x == 0) dtrace(A, 18 + l);   // accumulator of layer l ready
             tc_fence_after();
             constexpr int KPG = (KC8 + kGroups - 1) / kGroups;   // k-chunks per column group
             float v[KPG][8];
@@ -370,8 +410,17 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
             for (int kk = 0; kk < KPG; ++kk) {
                 const int kc = grp + kk * kGroups;
                 if (kc >= KC8) break;
+                if (valid) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[kk][e] = valid ? tanh_abs(v[kk][e]) : 0.f;
+                    for (int e = 0; e < 8; e += 2) {
+                        const float2 y = tanh_abs2(v[kk][e], v[kk][e + 1]);
+                        v[kk][e] = y.x;
+                        v[kk][e + 1] = y.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[kk][e] = 0.f;
+                }
                 uint4 hi, lo;
                 split8(v[kk], hi, lo);
                 st_shared_v4(act_hi + kc * LBO_A + (kPad + row) * 16, hi);
@@ -379,7 +428,8 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
             }
             tc_fence_before();
             fence_proxy_async_smem();
-            mbar_arrive(act_ready);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(act_ready);
         }
         // upsampler chunks: quantize, stage the row's piece, bulk-store it
         const bool out_row = row >= A.rf && row < A.rf + P && g < A.start + A.nout;
@@ -412,7 +462,8 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tmem_empty[buf]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[buf]);
             fence_proxy_async_smem();
             if (out_row && ncols > 0) {
                 int16_t *dst = A.out + (g - A.start) * A.hop + col0;
@@ -420,15 +471,20 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
                 bulk_commit();
             }
         }
-        bulk_wait0();
+        // the staging buffer must stay until the stores have READ it; their global writes
+        // complete before the kernel does
+        bulk_wait_read0();
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) dtrace(A, 31);
     if (warp == kEpiWarps + 1) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
 }
+
+static unsigned long long *g_dtrace = nullptr;   // debugging timeline (rf_decode_set_trace)
 
 // weights -> (hi, lo) fp16 blocks in the kernel's shared-memory operand layouts:
 //   conv layer l: [tap][piece][k/8][n = out channel][8]   (B[n][k] = kernels[l][tap][k][n])
@@ -566,6 +622,7 @@ extern "C" int rf_decode_window_tc(const double *latent, int64_t frames, int64_t
     A.cw = g.cw;
     A.nch = g.nch;
     A.out = out;
+    A.trace = g_dtrace;
     const int P = kRows - 2 * rfield;
     const int64_t tiles = (A.nout + P - 1) / P;
     // column slices: fill the SMs once (a slice recomputes its tile's conv stack)
@@ -582,3 +639,7 @@ extern "C" int rf_decode_window_tc(const double *latent, int64_t frames, int64_t
     RF_TRY_LAUNCH("rf_decode_tc_kernel");
     return RF_OK;
 }
+
+// Debugging aid (not part of the product ABI): globaltimer stamps of every decode CTA
+// ([cta][32] u64: phases of the conv stack / upsampler) -- see tools/decode_trace.py.
+extern "C" void rf_decode_set_trace(void *buf) { rf::dtc::g_dtrace = (unsigned long long *)buf; }
