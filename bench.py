@@ -218,7 +218,7 @@ def make_request(rf, stream_id):
 def forward_traffic():
     """DRAM bytes of one DiT forward from the committed ncu launch list (tools/forward_traffic.py)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_dit_forward_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r2_dit_forward_traffic.json")) as fh:
             t = json.load(fh)
         return t["warm"]["dram_bytes"], t["cold"]["dram_bytes"]
     except Exception:
@@ -557,7 +557,7 @@ def run_ours(args):
                      "achieved": round(agg_tflops, 1), "peak": round(world * bf16_sust, 1), "unit": "TFLOP/s",
                      "frac": round(agg_tflops / (world * bf16_sust), 4), "traffic": traffic_warm,
                      "traffic_note": "DRAM read+write bytes of one forward (sum over its launches) from the "
-                                     "committed ncu launch list profiles/r1_dit_forward_traffic.json, "
+                                     "committed ncu launch list profiles/r2_dit_forward_traffic.json, "
                                      f"--cache-control none; cold-cache sum {traffic_cold}",
                      "algorithmic_flops_per_launch": dit_flops,
                      "peak_source": f"{peak_src} bf16 sustained x {world} GPU(s) (burst {bf16_burst} per GPU)",
