@@ -13,8 +13,9 @@ for spec in "gateup:rf_gemm_kernel<\(int\)256, \(int\)3, \(int\)2" "down:rf_gemm
             "tick_solve:rf_tick_kernel" "decode:rf_decode_tc_kernel"; do
   n=${spec%%:*}; r=${spec#*:}
   if [ $n = tick_solve ]; then prog='python tools/toy_ticks.py 40'; elif [ $n = decode ]; then prog="python tools/decode_one.py 1500 1425 1500 4"; else prog=$P; fi
+  skip=12; if [ $n = decode ]; then skip=2; fi
   timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:$r" -s 12 -c 1 -o $O/$n $prog > $O/$n.log 2>&1
+    -k "regex:$r" -s $skip -c 1 -o $O/$n $prog > $O/$n.log 2>&1
 done
 M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:rf_|gemm -c 700 --csv"
 timeout 300 ncu $M --log-file $O/cold.csv $P > /dev/null 2>&1
