@@ -24,9 +24,12 @@ namespace rf {
 constexpr int kTickMaxRows = 32;
 constexpr int kTickMaxGroups = 4;  // channel groups of 64 per lane -> D <= 256
 
-struct TickBatch {
+// The rows travel as kernel parameters, sized to the launch (4, 8 or 32 rows): the launch
+// cost grows with the parameter block (7.7 KB at 32 rows), and a tick has `depth` rows.
+template <int CAP>
+struct TickBatchT {
     int count;
-    rf_row rows[kTickMaxRows];
+    rf_row rows[CAP];
 };
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -226,9 +229,9 @@ __device__ __forceinline__ void fast_pair(const rf_row &R, const double *__restr
     *(double2 *)(R.x + i) = make_double2(out[0], out[1]);
 }
 
-template <int LPF>
+template <int LPF, int CAP>
 __global__ void __launch_bounds__(256)
-rf_tick_kernel(const __grid_constant__ TickBatch B, int64_t T, int64_t D, const double *__restrict__ style) {
+rf_tick_kernel(const __grid_constant__ TickBatchT<CAP> B, int64_t T, int64_t D, const double *__restrict__ style) {
     const rf_row &R = B.rows[blockIdx.y];
     const int lane = threadIdx.x & 31;
     constexpr int FPW = 32 / LPF;  // frames per warp step
@@ -300,8 +303,8 @@ rf_tick_kernel(const __grid_constant__ TickBatch B, int64_t T, int64_t D, const 
     }
 }
 
-template <int LPF>
-static int launch_tick(const TickBatch &B, int64_t T, int64_t D, const double *style,
+template <int LPF, int CAP>
+static int launch_tick(const TickBatchT<CAP> &B, int64_t T, int64_t D, const double *style,
                        cudaStream_t st) {
     constexpr int FPW = 32 / LPF;
     const int warps_per_block = 8;
@@ -310,9 +313,25 @@ static int launch_tick(const TickBatch &B, int64_t T, int64_t D, const double *s
     // keep >= ~2 waves over the SMs across all rows without oversubscribing tiny rows
     if (bx < 1) bx = 1;
     dim3 grid((unsigned)bx, (unsigned)B.count);
-    rf_tick_kernel<LPF><<<grid, warps_per_block * 32, 0, st>>>(B, T, D, style);
+    rf_tick_kernel<LPF, CAP><<<grid, warps_per_block * 32, 0, st>>>(B, T, D, style);
     RF_TRY_LAUNCH("rf_tick_kernel");
     return RF_OK;
+}
+
+template <int CAP>
+static int launch_rows(const rf_row *rows, int n, int lpf, int64_t T, int64_t D, const double *style,
+                       cudaStream_t st) {
+    TickBatchT<CAP> B;
+    B.count = n;
+    for (int r = 0; r < n; ++r) B.rows[r] = rows[r];
+    switch (lpf) {
+        case 1: return launch_tick<1>(B, T, D, style, st);
+        case 2: return launch_tick<2>(B, T, D, style, st);
+        case 4: return launch_tick<4>(B, T, D, style, st);
+        case 8: return launch_tick<8>(B, T, D, style, st);
+        case 16: return launch_tick<16>(B, T, D, style, st);
+        default: return launch_tick<32>(B, T, D, style, st);
+    }
 }
 
 }  // namespace rf
@@ -373,18 +392,10 @@ extern "C" int rf_tick_solve(const rf_row *rows, int count, int64_t frames, int6
     int lpf = 1;
     while (lpf < half && lpf < 32) lpf <<= 1;
     for (int r0 = 0; r0 < count; r0 += kTickMaxRows) {
-        TickBatch B;
-        B.count = count - r0 < kTickMaxRows ? count - r0 : kTickMaxRows;
-        for (int r = 0; r < B.count; ++r) B.rows[r] = rows[r0 + r];
-        int rc;
-        switch (lpf) {
-            case 1: rc = launch_tick<1>(B, frames, channels, style_offset, st); break;
-            case 2: rc = launch_tick<2>(B, frames, channels, style_offset, st); break;
-            case 4: rc = launch_tick<4>(B, frames, channels, style_offset, st); break;
-            case 8: rc = launch_tick<8>(B, frames, channels, style_offset, st); break;
-            case 16: rc = launch_tick<16>(B, frames, channels, style_offset, st); break;
-            default: rc = launch_tick<32>(B, frames, channels, style_offset, st); break;
-        }
+        const int n = count - r0 < kTickMaxRows ? count - r0 : kTickMaxRows;
+        const int rc = n <= 4 ? launch_rows<4>(rows + r0, n, lpf, frames, channels, style_offset, st)
+                     : n <= 8 ? launch_rows<8>(rows + r0, n, lpf, frames, channels, style_offset, st)
+                              : launch_rows<kTickMaxRows>(rows + r0, n, lpf, frames, channels, style_offset, st);
         if (rc) return rc;
     }
     return RF_OK;
