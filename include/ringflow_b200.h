@@ -154,7 +154,8 @@ int rf_x0_compose(double *out, const double *base, const double *hint, double hs
  * with a fixed-order (deterministic) reduction.  `prev`/`reference` may be NULL.
  * Any count: emits run in launches of 16, each chunk's first prev being the previous
  * chunk's last latent.  scratch: device doubles owned by the caller (one buffer per
- * stream), at least rf_reduce_workspace_elems(numel). */
+ * stream), at least rf_reduce_workspace_elems(numel), ZEROED before its first use: its
+ * tail holds per-emit completion counters, which every call leaves zero again. */
 typedef struct rf_emit {
     const double *latent; /* slot state */
     double *record;       /* record-owned copy */

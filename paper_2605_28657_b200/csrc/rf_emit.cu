@@ -7,8 +7,8 @@
 namespace rf {
 
 constexpr int kRedThreads = 256;
-constexpr int kRedPerThread = 16;
-constexpr int kRedChunk = kRedThreads * kRedPerThread;  // elements per block
+constexpr int kRedPairs = 2;                             // double2 loads per thread
+constexpr int kRedChunk = kRedThreads * 2 * kRedPairs;  // elements per block (1024)
 constexpr int kMaxEmit = 16;
 constexpr int kMaxAdmit = 32;
 
@@ -28,8 +28,9 @@ __global__ void rf_admit_kernel(const __grid_constant__ AdmitBatch B, int64_t nu
     }
 }
 
-// Fixed-shape reduction tree: thread-sequential over 16 elements, then a fixed
-// shuffle/shared tree.  The result depends only on numel, never on timing.
+// Fixed-shape reduction tree: each thread sums its kRedPairs coalesced double2 pairs in
+// order, then a fixed shuffle/shared tree per block, then a fixed warp tree over the blocks'
+// partials.  The result depends only on numel, never on timing.
 __device__ __forceinline__ double block_sum(double v, double *sh) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
@@ -44,38 +45,67 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return r;
 }
 
+// one warp per emit: lane-strided sums of the block partials, then a fixed shuffle tree
+__device__ __forceinline__ double warp_sum_fixed(const double *part, int64_t chunks) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int64_t c = lane; c < chunks; c += 32) s = __dadd_rn(s, __ldcg(part + c));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+    return s;
+}
+
 struct EmitBatch {
     int count;
     rf_emit e[kMaxEmit];
 };
 
 // grid (chunks, emits): copy latent -> record, isfinite flag, chunk partials of
-// (lat - prev)^2 and (lat - ref)^2.
+// (lat - prev)^2 and (lat - ref)^2; the last block of each emit to finish (a counter per
+// emit, left zero again) sums that emit's partials with the fixed warp tree and writes its
+// mse values -- no second launch.
 __global__ void __launch_bounds__(kRedThreads)
 rf_emit_partials(const __grid_constant__ EmitBatch B, int64_t numel, const double *__restrict__ last,
                  const double *__restrict__ ref, double *__restrict__ part_prev,
-                 double *__restrict__ part_ref, uint32_t *__restrict__ status) {
+                 double *__restrict__ part_ref, uint32_t *__restrict__ status, unsigned int *__restrict__ done,
+                 double *__restrict__ mse_prev, double *__restrict__ mse_ref, int has_last) {
     __shared__ double sh[kRedThreads / 32];
+    __shared__ bool last_block;
     const int e = blockIdx.y;
     const double *lat = B.e[e].latent;
     double *rec = B.e[e].record;
     const double *prev = e == 0 ? last : B.e[e - 1].latent;
-    const int64_t base = (int64_t)blockIdx.x * kRedChunk + (int64_t)threadIdx.x * kRedPerThread;
+    // pair k of thread t: elements base + 2 (k * kRedThreads + t) + {0, 1} (coalesced)
+    const int64_t base = (int64_t)blockIdx.x * kRedChunk;
     double sp = 0.0, sr = 0.0;
     bool bad = false;
+    double lv[kRedPairs][2], pv[kRedPairs][2], rv[kRedPairs][2];
 #pragma unroll
-    for (int k = 0; k < kRedPerThread; ++k) {
-        int64_t i = base + k;
-        if (i < numel) {
-            double v = lat[i];
-            rec[i] = v;
+    for (int k = 0; k < kRedPairs; ++k) {   // every load first: one memory round trip
+        const int64_t i = base + 2 * ((int64_t)k * kRedThreads + threadIdx.x);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const bool in = i + h < numel;
+            lv[k][h] = in ? lat[i + h] : 0.0;
+            pv[k][h] = in && prev ? prev[i + h] : 0.0;
+            rv[k][h] = in && ref ? ref[i + h] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kRedPairs; ++k) {
+        const int64_t i = base + 2 * ((int64_t)k * kRedThreads + threadIdx.x);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (i + h >= numel) continue;
+            const double v = lv[k][h];
+            rec[i + h] = v;
             if (!isfinite(v)) bad = true;
             if (prev) {
-                double d = __dsub_rn(v, prev[i]);
+                double d = __dsub_rn(v, pv[k][h]);
                 sp = __dadd_rn(sp, __dmul_rn(d, d));
             }
             if (ref) {
-                double d = __dsub_rn(v, ref[i]);
+                double d = __dsub_rn(v, rv[k][h]);
                 sr = __dadd_rn(sr, __dmul_rn(d, d));
             }
         }
@@ -86,22 +116,21 @@ rf_emit_partials(const __grid_constant__ EmitBatch B, int64_t numel, const doubl
     if (threadIdx.x == 0) {
         part_prev[(int64_t)e * gridDim.x + blockIdx.x] = bp;
         part_ref[(int64_t)e * gridDim.x + blockIdx.x] = br;
+        __threadfence();
+        last_block = atomicAdd(done + e, 1u) == gridDim.x - 1;
     }
-}
-
-__global__ void rf_emit_finish(int count, int64_t chunks, int64_t numel, const double *part_prev,
-                               const double *part_ref, double *mse_prev, double *mse_ref, int has_last,
-                               int has_ref) {
-    const int e = threadIdx.x;
-    if (e >= count) return;
-    double sp = 0.0, sr = 0.0;
-    for (int64_t c = 0; c < chunks; ++c) {
-        sp = __dadd_rn(sp, part_prev[e * chunks + c]);
-        sr = __dadd_rn(sr, part_ref[e * chunks + c]);
+    __syncthreads();
+    if (!last_block || threadIdx.x >= 32) return;
+    __threadfence();
+    const int64_t chunks = gridDim.x;
+    const double tp = warp_sum_fixed(part_prev + e * chunks, chunks);
+    const double tr = warp_sum_fixed(part_ref + e * chunks, chunks);
+    if (threadIdx.x == 0) {
+        // prev of emit 0 is `last` (may be absent); later emits always have a prev
+        mse_prev[e] = (e == 0 && !has_last) ? -1.0 : __ddiv_rn(tp, (double)numel);
+        mse_ref[e] = ref ? __ddiv_rn(tr, (double)numel) : -1.0;
+        done[e] = 0u;   // ready for the next launch
     }
-    // prev of emit 0 is `last` (may be absent); later emits always have a prev
-    mse_prev[e] = (e == 0 && !has_last) ? -1.0 : __ddiv_rn(sp, (double)numel);
-    mse_ref[e] = has_ref ? __ddiv_rn(sr, (double)numel) : -1.0;
 }
 
 }  // namespace rf
@@ -163,7 +192,7 @@ extern "C" int rf_x0_compose(double *out, const double *base, const double *hint
 extern "C" int64_t rf_reduce_workspace_elems(int64_t numel) {
     if (numel <= 0) return 0;
     const int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
-    return 2 * chunks * kMaxEmit;
+    return 2 * chunks * kMaxEmit + kMaxEmit;   // partials, then kMaxEmit completion counters
 }
 
 extern "C" int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, const double *last,
@@ -182,6 +211,8 @@ extern "C" int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, con
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t chunks = (numel + kRedChunk - 1) / kRedChunk;
     double *pp = scratch, *pr = scratch + chunks * kMaxEmit;
+    // the per-emit completion counters (zero before the first call; every launch leaves them zero)
+    unsigned int *done = (unsigned int *)(scratch + 2 * chunks * kMaxEmit);
     for (int c0 = 0; c0 < count; c0 += kMaxEmit) {
         EmitBatch B;
         B.count = count - c0 < kMaxEmit ? count - c0 : kMaxEmit;
@@ -194,11 +225,8 @@ extern "C" int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, con
         }
         const double *prev = c0 == 0 ? last : emits[c0 - 1].latent;
         rf_emit_partials<<<dim3((unsigned)chunks, (unsigned)B.count), kRedThreads, 0, st>>>(
-            B, numel, prev, reference, pp, pr, status);
+            B, numel, prev, reference, pp, pr, status, done, mse_prev + c0, mse_ref + c0, prev != nullptr);
         RF_TRY_LAUNCH("rf_emit_partials");
-        rf_emit_finish<<<1, 32, 0, st>>>(B.count, chunks, numel, pp, pr, mse_prev + c0, mse_ref + c0,
-                                         prev != nullptr, reference != nullptr);
-        RF_TRY_LAUNCH("rf_emit_finish");
     }
     return RF_OK;
 }
@@ -208,14 +236,17 @@ __global__ void __launch_bounds__(kRedThreads)
 rf_sqdiff_partials(const double *__restrict__ a, const double *__restrict__ b, int64_t numel,
                    double *__restrict__ part) {
     __shared__ double sh[kRedThreads / 32];
-    const int64_t base = (int64_t)blockIdx.x * kRedChunk + (int64_t)threadIdx.x * kRedPerThread;
+    const int64_t base = (int64_t)blockIdx.x * kRedChunk;
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < kRedPerThread; ++k) {
-        int64_t i = base + k;
-        if (i < numel) {
-            double d = __dsub_rn(a[i], b[i]);
-            s = __dadd_rn(s, __dmul_rn(d, d));
+    for (int k = 0; k < kRedPairs; ++k) {
+        const int64_t i = base + 2 * ((int64_t)k * kRedThreads + threadIdx.x);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (i + h < numel) {
+                double d = __dsub_rn(a[i + h], b[i + h]);
+                s = __dadd_rn(s, __dmul_rn(d, d));
+            }
         }
     }
     double r = block_sum(s, sh);
@@ -223,9 +254,8 @@ rf_sqdiff_partials(const double *__restrict__ a, const double *__restrict__ b, i
 }
 
 __global__ void rf_sum_finish(const double *part, int64_t chunks, int64_t numel, double *out) {
-    double s = 0.0;
-    for (int64_t c = 0; c < chunks; ++c) s = __dadd_rn(s, part[c]);
-    *out = __ddiv_rn(s, (double)numel);
+    const double s = warp_sum_fixed(part, chunks);
+    if (threadIdx.x == 0) *out = __ddiv_rn(s, (double)numel);
 }
 
 extern "C" int rf_mse(const double *a, const double *b, int64_t numel, double *out, double *scratch,
@@ -242,7 +272,7 @@ extern "C" int rf_mse(const double *a, const double *b, int64_t numel, double *o
     }
     rf_sqdiff_partials<<<(unsigned)chunks, kRedThreads, 0, st>>>(a, b, numel, scratch);
     RF_TRY_LAUNCH("rf_sqdiff_partials");
-    rf_sum_finish<<<1, 1, 0, st>>>(scratch, chunks, numel, out);
+    rf_sum_finish<<<1, 32, 0, st>>>(scratch, chunks, numel, out);
     RF_TRY_LAUNCH("rf_sum_finish");
     return RF_OK;
 }

@@ -292,7 +292,8 @@ class StreamPipeline:
             self._stats_ptrs = (self._stats[0].data_ptr(), self._stats[1].data_ptr())
             # the emit reduction's partials: this pipeline's own (never shared across streams)
             self._reduce_elems = int(_native.load().rf_reduce_workspace_elems(T * D))
-            self._reduce_scratch = torch.empty(max(self._reduce_elems, 1), dtype=torch.float64, device=self._dev)
+            # zeroed once: its tail holds rf_emit_stats' completion counters (left zero by every call)
+            self._reduce_scratch = torch.zeros(max(self._reduce_elems, 1), dtype=torch.float64, device=self._dev)
         self.noise_cache = (NoiseCache(noise_cache_bytes, T * D, self._dev)
                             if noise_cache_bytes > 0 else None)
         self._emitbuf_host = torch.zeros(2 * nd + 1, dtype=torch.float64).pin_memory()
@@ -727,7 +728,7 @@ class StreamPipeline:
             self._reduce_elems, self._stream.cuda_stream),
             "rf_emit_stats")
         self._phase_end("emit", ev)
-        self.launches_last_tick += 2
+        self.launches_last_tick += 1
         self._emitbuf_host.copy_(self._emitbuf, non_blocking=True)
         done = self._emit_event
         done.record(self._stream)

@@ -136,9 +136,9 @@ def test_launch_count_and_no_sync_without_emit(rf, cache):
     assert sorted(c for c, _ in counts) == [0, 0, 1, 1]
     for n_emit, launches in counts:
         if cache:   # every draw hits: solve (+ emit statistics + admission init)
-            assert launches == 1 + (2 + 1 if n_emit else 0)
-        else:       # noise (2) + solve (+ emit (2) + admission noise (2) + init)
-            assert launches == 3 + (2 + 3 if n_emit else 0)
+            assert launches == 1 + (1 + 1 if n_emit else 0)
+        else:       # noise (2) + solve (+ emit (1) + admission noise (2) + init)
+            assert launches == 3 + (1 + 3 if n_emit else 0)
 
 
 def test_backpressure_and_errors(rf):
