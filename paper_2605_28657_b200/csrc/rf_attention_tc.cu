@@ -411,8 +411,14 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
     uint64_t *qfull = bar, *kfull = bar + 1, *kempty = kfull + KS, *vfull = kempty + KS, *vempty = vfull + KS;
     uint64_t *sfull = vempty + KS;         // [head * 2 + buffer]
     // odone[head * 2 + (j & 1)]: PV(j) completion, alternating by tile parity so a waiter that
-    // skipped phases still reads an unambiguous parity (see the rescale wait below)
-    uint64_t *pfull = sfull + 2 * NH, *odone = pfull + NH;
+    // skipped phases still reads an unambiguous parity (see the rescale wait below).
+    // pfull[head * 2 + (j & 1)]: P(j) written, alternating by tile parity too: the softmax can
+    // finish tiles j AND j + 1 (S(j + 1) is issued before the MMA warp waits for P(j)) before
+    // the MMA warp first polls, and one barrier would then be two phases ahead of its waiter,
+    // whose parity wait can never succeed (a hang caught by the RF_HANG_TRAP build).  With a
+    // barrier per parity, P(j + 2) -- which needs S(j + 2), issued only after the wait -- is
+    // the earliest that could complete the waited barrier's next phase.
+    uint64_t *pfull = sfull + 2 * NH, *odone = pfull + 2 * NH;
     uint32_t *tmem_slot = (uint32_t *)(odone + 2 * NH);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -437,7 +443,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             mbar_init(&vempty[i], 1);
         }
         for (int i = 0; i < 2 * NH; ++i) mbar_init(&sfull[i], 1);
-        for (int i = 0; i < NH; ++i) mbar_init(&pfull[i], 4);   // the 4 softmax warps of the head
+        for (int i = 0; i < 2 * NH; ++i) mbar_init(&pfull[i], 4);   // the 4 softmax warps of the head
         for (int i = 0; i < 2 * NH; ++i) mbar_init(&odone[i], 1);
         mbar_fence_init();
     }
@@ -504,7 +510,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
                 const int s = j % KS, s2 = (j + 2) % KS, buf = j & 1;
 #pragma unroll 1
                 for (int a = 0; a < NH; ++a) {
-                    mbar_wait(&pfull[a], j & 1);
+                    mbar_wait(&pfull[a * 2 + (j & 1)], (j >> 1) & 1);
                     if (a == 0) mbar_wait(&vfull[s], (j / KS) & 1);
                     tc_fence_after();
                     FA_TRACE(a, j);
@@ -599,7 +605,7 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&pfull[a]);
+            if (lane == 0) mbar_arrive(&pfull[a * 2 + (j & 1)]);
             // keep the head's 4 warps within one tile of each other: pfull counts 4 arrivals per
             // phase, so a warp that raced ahead and arrived for tile j + 1 before a slow warp's
             // tile-j arrival would complete phase j early (PV(j) reading unfinished P rows)

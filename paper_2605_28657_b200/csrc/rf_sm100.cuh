@@ -1,6 +1,7 @@
 // Blackwell (sm_100a) primitives as inline PTX: mbarriers, TMA, tcgen05 / TMEM.
 // Used by the tensor-core kernels of the DiT (GEMM, attention).
 #pragma once
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -39,6 +40,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity), "n"(RF_WAIT_HINT)
         : "memory");
+#elif defined(RF_HANG_TRAP)
+    // diagnostic build only (tools/hang_diag.sh): a wait that has not completed after ~4 s
+    // reports the kernel's grid position, the barrier and the phase, and traps
+    const long long t0 = clock64();
+    for (uint32_t n = 0;; ++n) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (ok) break;
+        if ((n & 1023) == 0 && clock64() - t0 > 8000000000ll) {
+            printf("RF_HANG grid (%d,%d) block (%d,%d) of %d threads, thread %d smem bar 0x%x parity %u\n",
+                   gridDim.x, gridDim.y, blockIdx.x, blockIdx.y, blockDim.x, threadIdx.x, smem_u32(bar), parity);
+            __trap();
+        }
+    }
 #else
     asm volatile(
         "{\n"

@@ -218,3 +218,38 @@ def test_stream_group_batches_rows_bit_identically(dit_mod, full):
         assert len(a) == len(b) >= 3
         for (ta, sa, la), (tb, sb, lb) in zip(a, b):
             assert ta == tb and sa == sb and np.array_equal(la, lb)
+
+
+def test_attention_under_concurrent_load(dit_mod):
+    """The self-attention kernel, launched back to back while another stream keeps the SMs
+    busy (as the trajectory tests' oracle does): every launch completes and matches the
+    first.  Its P-ready barriers alternate by key-tile parity -- with one barrier the softmax
+    warps could finish two tiles before the MMA warp polled, leaving the waiter two phases
+    behind (an intermittent hang, caught by the RF_HANG_TRAP diagnostic build)."""
+    import ctypes
+
+    from paper_2605_28657_b200 import _native
+
+    lib = _native.load()
+    B, N, H, Hk = 4, 750, 16, 8
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn(B * N, H * 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B * N, Hk * 128, device="cuda", generator=g).bfloat16()
+    vt = torch.randn(B, Hk, 128, (N + 7) // 8 * 8, device="cuda", generator=g).bfloat16()
+    vt[..., N:] = 0
+    outs = [torch.empty(B * N, H * 128, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    side, main = torch.cuda.Stream(), torch.cuda.Stream()
+    a = torch.randn(2048, 2048, device="cuda")
+    for it in range(6):
+        with torch.cuda.stream(side):
+            for _ in range(20):
+                a = torch.tanh(a @ a * 1e-3)
+        with torch.cuda.stream(main):
+            for r in range(50):
+                _native.check(lib.rf_attention_tc_bf16_kernel(
+                    0, vp(q.data_ptr()), vp(k.data_ptr()), vp(vt.data_ptr()), vp(outs[r % 2].data_ptr()), B, N, N,
+                    vt.shape[-1], H, Hk, i64(H * 128), i64(Hk * 128), i64(H * 128), vp(main.cuda_stream)), "attention")
+        main.synchronize()
+        assert torch.equal(outs[0], outs[1])
+    side.synchronize()
