@@ -44,7 +44,7 @@ struct L2Window {
     size_t bytes = 0;
     float hit_ratio = 0.f;
 };
-inline L2Window g_l2_window;
+inline thread_local L2Window g_l2_window;   // set per thread while a DiT forward is launched / captured
 
 // appends the window attribute (if any) to at[n]; returns the new attribute count
 inline unsigned add_l2_window(cudaLaunchAttribute *at, unsigned n) {

@@ -19,6 +19,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <mutex>
 #include <vector>
 
 #include "rf_common.cuh"
@@ -29,6 +30,11 @@
 namespace rf {
 
 constexpr int kMaxDitRows = 64;
+
+// live DiT handles holding the device's persisting-L2 set-aside, and the limit before the first
+static std::mutex g_l2_mu;
+static int g_l2_users = 0;
+static size_t g_l2_saved = 0;
 
 // ------------------------------------------------------------------ kernels ------
 // RMSNorm over d (fp32 residual row) with optional AdaLN modulation, bf16 out.
@@ -373,18 +379,25 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         delete d;
         return rc;
     }
-    // L2 persistence for the fp32 residual stream (24.6 MB at 4 rows; +1.2%)
+    // L2 persistence for the fp32 residual stream (24.6 MB at 4 rows; +1.2%).
+    // The set-aside is device-wide state: the first live DiT saves the previous limit and the
+    // last one destroyed restores it (other work on the device gets its L2 back).
     {
         int dev = 0, maxp = 0;
         const size_t hb = (size_t)max_rows * d->tokens * c.d_model * sizeof(float);
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && maxp > 0) {
+            std::lock_guard<std::mutex> g(g_l2_mu);
             size_t lim = hb < (size_t)maxp ? hb : (size_t)maxp, cur = 0;
-            if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur > lim) lim = cur;
-            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim) == cudaSuccess) {
-                d->l2win.base = d->h;
-                d->l2win.bytes = hb;
-                d->l2win.hit_ratio = lim >= hb ? 1.0f : (float)lim / (float)hb;
+            if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess) {
+                if (g_l2_users == 0) g_l2_saved = cur;
+                if (cur > lim) lim = cur;
+                if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim) == cudaSuccess) {
+                    d->l2win.base = d->h;
+                    d->l2win.bytes = hb;
+                    d->l2win.hit_ratio = lim >= hb ? 1.0f : (float)lim / (float)hb;
+                    ++g_l2_users;
+                }
             }
         }
         cudaGetLastError();   // attribute / limit queries are best-effort
@@ -400,9 +413,18 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
 
 extern "C" int rf_dit_destroy(void *handle) {
     Dit *d = (Dit *)handle;
-    if (d)
+    if (d) {
         for (auto &g : d->graph)
             if (g) cudaGraphExecDestroy(g);
+        if (d->l2win.base) {
+            std::lock_guard<std::mutex> g(g_l2_mu);
+            if (--g_l2_users == 0) {   // the last DiT: give the set-aside back
+                cudaCtxResetPersistingL2Cache();
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_saved);
+                cudaGetLastError();
+            }
+        }
+    }
     delete d;
     return RF_OK;
 }
