@@ -65,4 +65,3 @@ def main():
 
 if __name__ == "__main__":
     main()
-print("step_slots sections (us/tick):", [round(x / 464 * 1e6, 1) for x in P._SECT])
