@@ -132,6 +132,9 @@ int gemm_plan(GemmPlan *p, const void *A, const void *B, int64_t M, int64_t N, i
 }
 
 static unsigned long long *g_trace = nullptr;   // debugging timeline buffer (rf_gemm_set_trace)
+// sequential mode (rf_gemm_set_trace_seq): launch i gets its own [cta][16][8] block
+static int64_t g_trace_seq_max = 0, g_trace_seq_next = 0;
+constexpr int64_t kTraceBlock = 400 * 16 * 8;
 
 int gemm_plan_c(GemmPlan *p, void *out, int64_t ldo) {
     p->c_ptr = out;
@@ -168,6 +171,8 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
     gemm::EpiArgs e{out, ldo, gate, gate_ld, rows_per_batch > 0 ? rows_per_batch : 1, alpha, rope, rope_cols,
                     vt ? (__nv_bfloat16 *)vt->ptr : nullptr, vt ? vt->col0 : 0, vt ? vt->heads : 0,
                     vt ? vt->ld : 0, vt ? vt->period : 0, vt ? vt->layer_stride : 0, g_trace};
+    if (g_trace && g_trace_seq_max > 0)   // each launch (also each captured graph node) its own block
+        e.trace = g_trace_seq_next < g_trace_seq_max ? g_trace + kTraceBlock * g_trace_seq_next++ : nullptr;
     if (nf) {
         if ((nf->aux && epi != gemm::kResidGate) || (nf->rs_part && epi != gemm::kStoreBF16 && epi != gemm::kCrossAttn)) {
             set_error("gemm: fused norm needs a gated-residual producer / bf16-store consumer");
@@ -211,7 +216,20 @@ using namespace rf;
 
 // Debugging aid (not part of the product ABI): when set, every GEMM launch records a
 // clock64 timeline per CTA into buf ([cta][tile < 16][8] u64) -- see tools/gemm_trace.py.
-extern "C" void rf_gemm_set_trace(void *buf) { g_trace = (unsigned long long *)buf; }
+extern "C" void rf_gemm_set_trace(void *buf) {
+    g_trace = (unsigned long long *)buf;
+    g_trace_seq_max = 0;
+}
+// Debugging aid: every GEMM launched (or captured into a graph) from now on records its
+// per-CTA entry / exit globaltimer stamps in its own block of buf ([launch][400][16][8] u64,
+// entry at [cta][15][7], exit at [cta][14][7]) -- the in-situ timeline of a DiT forward
+// (tools/forward_timeline.py).  Returns the launch index the next GEMM will get.
+extern "C" int64_t rf_gemm_set_trace_seq(void *buf, int64_t max_launches) {
+    g_trace = (unsigned long long *)buf;
+    g_trace_seq_max = buf ? max_launches : 0;
+    g_trace_seq_next = 0;
+    return 0;
+}
 
 extern "C" int rf_gemm_bf16(const void *A, const void *B, void *out, int64_t M, int64_t N, int64_t K,
                             int64_t lda, int64_t ldb, int64_t ldo, int32_t epilogue, const float *gate,
