@@ -31,10 +31,11 @@ namespace rf {
 
 constexpr int kMaxDitRows = 64;
 
-// live DiT handles holding the device's persisting-L2 set-aside, and the limit before the first
+// per device: live DiT handles holding its persisting-L2 set-aside, and the limit before the first
+constexpr int kMaxDevices = 64;
 static std::mutex g_l2_mu;
-static int g_l2_users = 0;
-static size_t g_l2_saved = 0;
+static int g_l2_users[kMaxDevices] = {};
+static size_t g_l2_saved[kMaxDevices] = {};
 
 // ------------------------------------------------------------------ kernels ------
 // RMSNorm over d (fp32 residual row) with optional AdaLN modulation, bf16 out.
@@ -197,6 +198,7 @@ struct Dit {
     int graph_kernels[kMaxDitRows + 1] = {};   // kernel nodes of each captured forward
     float *graph_out[kMaxDitRows + 1] = {};
     L2Window l2win;   // the residual stream h, kept persisting in L2 during the forward
+    int device = -1;  // the device whose persisting-L2 limit this handle raised (-1: none)
     // GEMM plans (tensor maps at max rows)
     GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out, p_kvc;
     std::vector<GemmPlan> p_qkv, p_o, p_qc, p_oc, p_gu, p_down;
@@ -385,18 +387,19 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     {
         int dev = 0, maxp = 0;
         const size_t hb = (size_t)max_rows * d->tokens * c.d_model * sizeof(float);
-        if (cudaGetDevice(&dev) == cudaSuccess &&
+        if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < kMaxDevices &&
             cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && maxp > 0) {
             std::lock_guard<std::mutex> g(g_l2_mu);
             size_t lim = hb < (size_t)maxp ? hb : (size_t)maxp, cur = 0;
             if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess) {
-                if (g_l2_users == 0) g_l2_saved = cur;
+                if (g_l2_users[dev] == 0) g_l2_saved[dev] = cur;
                 if (cur > lim) lim = cur;
                 if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim) == cudaSuccess) {
                     d->l2win.base = d->h;
                     d->l2win.bytes = hb;
                     d->l2win.hit_ratio = lim >= hb ? 1.0f : (float)lim / (float)hb;
-                    ++g_l2_users;
+                    d->device = dev;
+                    ++g_l2_users[dev];
                 }
             }
         }
@@ -416,11 +419,15 @@ extern "C" int rf_dit_destroy(void *handle) {
     if (d) {
         for (auto &g : d->graph)
             if (g) cudaGraphExecDestroy(g);
-        if (d->l2win.base) {
+        if (d->device >= 0) {
             std::lock_guard<std::mutex> g(g_l2_mu);
-            if (--g_l2_users == 0) {   // the last DiT: give the set-aside back
+            if (--g_l2_users[d->device] == 0) {   // the device's last DiT: give the set-aside back
+                int cur = -1;
+                cudaGetDevice(&cur);
+                if (cur != d->device) cudaSetDevice(d->device);
                 cudaCtxResetPersistingL2Cache();
-                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_saved);
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_saved[d->device]);
+                if (cur >= 0 && cur != d->device) cudaSetDevice(cur);
                 cudaGetLastError();
             }
         }
