@@ -18,6 +18,7 @@ the oracle the DiT is tested against (DiT parity is unpinned by the reference it
 from __future__ import annotations
 
 import ctypes
+import threading
 import math
 from dataclasses import dataclass, field
 
@@ -177,6 +178,9 @@ class DiT:
         # One event per stream that used them; the allocator is told about every such
         # stream (record_stream), so their memory is not reused before that work is done.
         self._busy: dict = {}
+        # host-side state of the handle (row table, captured graphs per row count) is built
+        # and replayed by one thread at a time
+        self._lock = threading.Lock()
         # weights, tables and the handle were initialised on the creating stream: complete
         # them before any other stream can touch them
         torch.cuda.current_stream(self.dev).synchronize()
@@ -243,13 +247,14 @@ class DiT:
         if n > self.max_rows:
             raise ValueError(f"{n} rows > max_rows {self.max_rows}")
         out = self.out if out is None else out
-        self._order_after_previous_use()
         xp = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
         tp = (ctypes.c_float * n)(*[float(t) for t in ts])
         cp = (ctypes.c_void_p * n)(*[c.data_ptr() for c in conds])
-        _native.check(self.lib.rf_dit_forward(self.handle, n, xp, tp, cp, out.data_ptr(),
-                                              _device.current_stream_handle()), "rf_dit_forward")
-        self.mark_used()
+        with self._lock:
+            self._order_after_previous_use()
+            _native.check(self.lib.rf_dit_forward(self.handle, n, xp, tp, cp, out.data_ptr(),
+                                                  _device.current_stream_handle()), "rf_dit_forward")
+            self.mark_used()
         return out[:n]
 
 
