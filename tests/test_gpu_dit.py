@@ -253,3 +253,34 @@ def test_attention_under_concurrent_load(dit_mod):
         main.synchronize()
         assert torch.equal(outs[0], outs[1])
     side.synchronize()
+
+
+def test_persisting_l2_set_aside_is_returned(dit_mod):
+    """A DiT raises the device's persisting-L2 limit for its residual stream; when the last
+    DiT on the device is destroyed the previous limit is back (other work gets its L2)."""
+    import gc
+
+    before = _persisting_limit()
+    a = dit_mod.DiT(dit_mod.DiTConfig().small(), frames=96, max_rows=2)
+    b = dit_mod.DiT(dit_mod.DiTConfig().small(), frames=96, max_rows=2)
+    assert _persisting_limit() >= before
+    del a
+    gc.collect()
+    del b
+    gc.collect()
+    torch.cuda.synchronize()
+    assert _persisting_limit() == before
+
+
+def _persisting_limit() -> int:
+    """cudaDeviceGetLimit(cudaLimitPersistingL2CacheSize) on the current device (cuda-python)."""
+    try:
+        from cuda.bindings import runtime as cudart
+    except ImportError:
+        try:
+            from cuda import cudart
+        except ImportError:
+            pytest.skip("cuda-python runtime bindings not importable")
+    err, v = cudart.cudaDeviceGetLimit(cudart.cudaLimit.cudaLimitPersistingL2CacheSize)
+    assert int(err) == 0, err
+    return int(v)
