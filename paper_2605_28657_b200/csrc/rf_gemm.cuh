@@ -623,9 +623,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         uint32_t acc_phase = 0;
         for (Walk w = walk_init(); walk_next(w, t, kb0, kb1); ++it) {
             const int n0 = (t / num_m) * BN;
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            if (q == 2 && lane == 0) RF_TRACE(it, 4);
             {
             const int m0 = row0(t);
             const int m = m0 + q * 32 + lane;
@@ -642,7 +639,9 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             // (8 float4) per 32-column chunk.  Chunks h * 128 + pb * 32 of the tile's heads
             // share block pb, so chunks are walked pb-major and block pb + 1 is prefetched
             // while block pb is applied (the table row is an L2 read; a load per use
-            // stalled the epilogue behind the main loop).
+            // stalled the epilogue behind the main loop).  Blocks 0 and 1 are loaded before
+            // the accumulator wait, so their latency hides behind the tile's main loop (the
+            // Q / K tiles' epilogue was longer than their main loop: tools/forward_timeline.py).
             constexpr int NCH = BN / 32;
             constexpr int NH = EPI == kBF16Rope ? BN / 128 : 1;
             if constexpr (C::TMA_O) {   // the previous tile's stores have read the staging buffer
@@ -658,17 +657,22 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 if (tile_rot) {
 #pragma unroll
                     for (int v = 0; v < 8; ++v) tc[v] = __ldg(tab + v);
+                    if (NH < NCH) {
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) tn[v] = __ldg(tab + 8 + v);
+                    }
                 }
             }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            if (q == 2 && lane == 0) RF_TRACE(it, 4);
 #pragma unroll 1
             for (int ci = 0; ci < NCH; ++ci) {
                 const int c0 = EPI == kBF16Rope ? (ci % NH) * 128 + (ci / NH) * 32 : ci * 32;
                 if constexpr (EPI == kBF16Rope) {
-                    if (tile_rot && ci % NH == 0) {
-                        if (ci > 0) {
+                    if (tile_rot && ci % NH == 0 && ci > 0) {   // block ci / NH is in tn
 #pragma unroll
-                            for (int v = 0; v < 8; ++v) tc[v] = tn[v];
-                        }
+                        for (int v = 0; v < 8; ++v) tc[v] = tn[v];
                         if (ci + NH < NCH) {
 #pragma unroll
                             for (int v = 0; v < 8; ++v) tn[v] = __ldg(tab + (ci / NH + 1) * 8 + v);

@@ -66,6 +66,39 @@ def main():
         print(f"  {k:10s} work {sum(dur[k]) / len(dur[k]):7.2f} us   gap before {sum(gap['before ' + k]) / 24:6.2f} us")
     print("  (gap before qkv = norm1 (+ launch); before o = self-attention; before gate_up = norm3; "
           "before o_cross = 0 (xattn fused); before xq+xattn: the O-proj -> cross-Q handoff)")
+    # per-tile clock64 stamps of the same launches (MMA warp of the leader CTAs: 0 tile start,
+    # 1 accumulator free, 2 first operands, 3 all k blocks issued; epilogue warp: 4 accumulator
+    # full, 5 done) -- is each GEMM kind fed, or waiting for its epilogue?
+    print("  per tile (cycles, mean over layers):  acc-wait  operand-wait  issue-span  epilogue")
+    for k in range(per):
+        aw, ow, sp, ep = [], [], [], []
+        for li in range(24):
+            blk_ = t[launches[6 + li * per + k]]
+            for c in range(400):
+                for it in range(16):
+                    st = blk_[c, it]
+                    if st[0] and st[1] and st[2] and st[3]:
+                        aw.append(st[1] - st[0])
+                        ow.append(st[2] - st[1])
+                        sp.append(st[3] - st[2])
+                    if st[4] and st[5]:
+                        ep.append(st[5] - st[4])
+        m = lambda v: sum(v) / len(v) if v else float("nan")  # noqa: E731
+        print(f"  {names[k]:10s} {m(aw):9.0f} {m(ow):13.0f} {m(sp):11.0f} {m(ep):9.0f}")
+    # QKV: epilogue by column block kind (tile = unit + k * 74, 12 m-blocks, 16 n-blocks of
+    # 256: Q 0-7 with RoPE, K 8-11 with RoPE, V 12-15 written transposed)
+    kinds = {"q": [], "k": [], "v": []}
+    for li in range(24):
+        blk_ = t[launches[6 + li * per]]
+        for c in range(0, 400):
+            for it in range(16):
+                st = blk_[c, it]
+                if st[4] and st[5]:
+                    tile = (c >> 1) + it * 74
+                    nb = tile // 12
+                    kinds["q" if nb < 8 else "k" if nb < 12 else "v"].append(st[5] - st[4])
+    print("  qkv epilogue by block kind: " + ", ".join(f"{k} {sum(v) / max(len(v), 1):.0f} cycles (n={len(v)})"
+                                                      for k, v in kinds.items()))
 
 
 if __name__ == "__main__":
