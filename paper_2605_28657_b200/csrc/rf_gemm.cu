@@ -103,7 +103,11 @@ static int dispatch(const GemmPlan &p, int epi, const gemm::EpiArgs &e, cudaStre
             if constexpr (BN == 256) {
                 return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
             } else {
-                if (p.K >= 4096) return launch<BN, gemm::kResidGate, CG, 64>(p, e, st);
+                // long K (the down projection, K = 6144): the residual staged 32 columns per
+                // pass leaves room for an 8th operand stage, which the 96-k-block main loop's
+                // feed needs more than the epilogue needs the staging (61.2 vs 62.9 us
+                // standalone, profiles/r2_gemm_trace.txt); K = 2048 keeps one 128-column pass
+                if (p.K >= 4096) return launch<BN, gemm::kResidGate, CG, 32>(p, e, st);
                 return launch<BN, gemm::kResidGate, CG>(p, e, st);
             }
         case gemm::kSwiGLU: return launch<BN, gemm::kSwiGLU, CG>(p, e, st);
