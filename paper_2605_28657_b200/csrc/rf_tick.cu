@@ -161,13 +161,14 @@ __device__ __forceinline__ double group_sum(double v) {
     return v;
 }
 
-// The common row (one condition, no guidance, SDE step, no morph target): the same
-// operations in the same order as velocity_elem + solve_elem, but every operand of a
-// lane's two channels is fetched with one 16-byte (8-byte for fp32 velocities) load,
-// all of them issued before any arithmetic, so a thread makes one memory round trip
-// instead of a chain of dependent scalar loads.  The kernel is HBM-bound; this is what
-// lets it approach the roofline (bench.py toy_path.solver_roofline).
-__device__ __forceinline__ bool fast_row(const rf_row &R, int64_t D) {
+// The common row (one condition, no guidance, SDE step, no morph target) runs in its own
+// lean kernel: the same operations in the same order as velocity_elem + solve_elem, on
+// channel PAIRS (16-byte loads; 8-byte for fp32 velocities) indexed flat over the row, every
+// operand of a thread's PPT pairs loaded before any arithmetic.  Split from the general
+// kernel because register allocation is per kernel: the general path's 80 registers left
+// 3 blocks per SM and 1.7 waves for the common case, which is HBM-bound and wants the whole
+// launch resident in one wave with every load in flight (bench.py toy_path.solver_roofline).
+__host__ __device__ inline bool fast_row(const rf_row &R, int64_t D) {
     const uintptr_t al = (uintptr_t)R.x | (uintptr_t)R.cond_x0[0] | (uintptr_t)R.noise_step |
                          (uintptr_t)R.source | (uintptr_t)R.noise_model;
     const uintptr_t need = (R.flags & RF_ROWF_V_F32) ? 7 : 15;
@@ -177,56 +178,95 @@ __device__ __forceinline__ bool fast_row(const rf_row &R, int64_t D) {
            ((al & need) == 0);
 }
 
+// the fields of a fast row (88 bytes instead of rf_row's 248: a smaller parameter block)
+struct FastRow {
+    double *x;
+    const void *v;             // cond_x0[0]: velocity (fp32 / fp64) or the toy x0 partial
+    const double *nm;          // model noise or null
+    const double *n;           // SDE noise
+    const double *src;         // source or null
+    const double *csde;        // per-frame SDE blend curve or null (= 1)
+    double tc, tn, jt;
+    int32_t flags;
+};
+template <int CAP>
+struct FastBatchT {
+    int count;
+    uint32_t half_d;           // channel pairs per frame
+    uint32_t pairs;            // channel pairs per row (T * D / 2)
+    FastRow rows[CAP];
+};
+
 __device__ __forceinline__ double2 ld2(const double *p) { return __ldg((const double2 *)p); }
 
-__device__ __forceinline__ void fast_pair(const rf_row &R, const double *__restrict__ style, int64_t f, int64_t i) {
-    const double2 x = *(const double2 *)(R.x + i);
-    const bool cond_v = (R.flags & RF_ROWF_COND_V) != 0;
-    double2 vg = make_double2(0.0, 0.0), x0p = vg, st = vg, nm = vg, src = vg;
-    if (cond_v) {
-        if (R.flags & RF_ROWF_V_F32) {
-            const float2 v32 = __ldg((const float2 *)R.cond_x0[0] + i / 2);
-            vg = make_double2((double)v32.x, (double)v32.y);
-        } else {
-            vg = ld2(R.cond_x0[0] + i);
-        }
-        if (R.flags & RF_ROWF_STYLE_V) st = ld2(style + i);
-    } else {
-        x0p = ld2(R.cond_x0[0] + i);
-        st = ld2(style + i);
-        if (R.noise_model) nm = ld2(R.noise_model + i);
-    }
-    const double2 n = ld2(R.noise_step + i);
-    if (R.source) src = ld2(R.source + i);
-    const double c = R.source ? curve_or(R.curves[RF_CURVE_SDE], f, 1.0) : 1.0;
-    const double tc = R.t_curr, tn = R.t_next;
-    const double xv[2] = {x.x, x.y}, vgv[2] = {vg.x, vg.y}, x0v[2] = {x0p.x, x0p.y}, sv[2] = {st.x, st.y},
-                 nmv[2] = {nm.x, nm.y}, nv[2] = {n.x, n.y}, srcv[2] = {src.x, src.y};
-    double out[2];
+// One channel pair per thread, <= 64 registers (4 blocks of 256 per SM): 752 blocks for a
+// config-2 tick, one wave.  Measured equal within noise to 2 pairs per thread (73 registers,
+// 3 blocks per SM), 128-thread blocks and <= 40 registers; 4 pairs per thread +22%
+// (profiles/r2_solver.txt).  The launch is latency-bound at this size (21.5 MB algorithmic,
+// 11.5 MB from DRAM: the source, x0 table and style offset are shared by the rows).
+constexpr int kFastThreads = 256;
+constexpr int kFastPPT = 1;    // channel pairs per thread
+constexpr int kFastMinBlocks = 4;
+
+template <int CAP>
+__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks)
+rf_tick_fast_kernel(const __grid_constant__ FastBatchT<CAP> B, const double *__restrict__ style) {
+    const FastRow &R = B.rows[blockIdx.y];
+    const bool cond_v = (R.flags & RF_ROWF_COND_V) != 0, v32 = (R.flags & RF_ROWF_V_F32) != 0;
+    const bool sty = !cond_v || (R.flags & RF_ROWF_STYLE_V);
+    double2 x[kFastPPT], vg[kFastPPT], st[kFastPPT], nm[kFastPPT], n[kFastPPT], src[kFastPPT];
+    double c[kFastPPT];
+    uint32_t p[kFastPPT];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        double v;
-        if (cond_v) {
-            v = vgv[e];
-            if (R.flags & RF_ROWF_STYLE_V) v = dsub(v, ddiv(sv[e], tc));
-        } else {   // toy_velocity
-            const double x0 = dadd(x0v[e], sv[e]);
-            v = ddiv(dsub(xv[e], x0), tc);
-            if (R.noise_model) v = dadd(v, dmul(R.jitter_t, nmv[e]));
-        }
-        // solve_elem, SDE, no morph
-        const double x0pe = dsub(xv[e], dmul(v, tc));
-        const double tnn = dmul(tn, nv[e]);
-        const double omt = dsub(1.0, tn);
-        const double full = dadd(tnn, dmul(omt, x0pe));
-        if (!R.source) {
-            out[e] = full;
+    for (int k = 0; k < kFastPPT; ++k) {
+        p[k] = (blockIdx.x * kFastPPT + k) * kFastThreads + threadIdx.x;
+        if (p[k] >= B.pairs) continue;
+        const uint32_t i = 2 * p[k];
+        x[k] = *(const double2 *)(R.x + i);
+        if (cond_v && v32) {
+            const float2 w = __ldg((const float2 *)R.v + p[k]);
+            vg[k] = make_double2((double)w.x, (double)w.y);
         } else {
-            const double sr = dadd(tnn, dmul(omt, srcv[e]));
-            out[e] = dadd(dmul(c, full), dmul(dsub(1.0, c), sr));
+            vg[k] = ld2((const double *)R.v + i);
         }
+        st[k] = sty ? ld2(style + i) : make_double2(0.0, 0.0);
+        nm[k] = R.nm ? ld2(R.nm + i) : make_double2(0.0, 0.0);
+        n[k] = ld2(R.n + i);
+        src[k] = R.src ? ld2(R.src + i) : make_double2(0.0, 0.0);
+        c[k] = (R.src && R.csde) ? __ldg(R.csde + p[k] / B.half_d) : 1.0;
     }
-    *(double2 *)(R.x + i) = make_double2(out[0], out[1]);
+    const double tc = R.tc, tn = R.tn;
+#pragma unroll
+    for (int k = 0; k < kFastPPT; ++k) {
+        if (p[k] >= B.pairs) continue;
+        const double xv[2] = {x[k].x, x[k].y}, gv[2] = {vg[k].x, vg[k].y}, sv[2] = {st[k].x, st[k].y},
+                     nmv[2] = {nm[k].x, nm[k].y}, nv[2] = {n[k].x, n[k].y}, srcv[2] = {src[k].x, src[k].y};
+        double out[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double v;
+            if (cond_v) {
+                v = gv[e];
+                if (R.flags & RF_ROWF_STYLE_V) v = dsub(v, ddiv(sv[e], tc));
+            } else {   // toy_velocity
+                const double x0 = dadd(gv[e], sv[e]);
+                v = ddiv(dsub(xv[e], x0), tc);
+                if (R.nm) v = dadd(v, dmul(R.jt, nmv[e]));
+            }
+            // solve_elem, SDE, no morph
+            const double x0pe = dsub(xv[e], dmul(v, tc));
+            const double tnn = dmul(tn, nv[e]);
+            const double omt = dsub(1.0, tn);
+            const double full = dadd(tnn, dmul(omt, x0pe));
+            if (!R.src) {
+                out[e] = full;
+            } else {
+                const double sr = dadd(tnn, dmul(omt, srcv[e]));
+                out[e] = dadd(dmul(c[k], full), dmul(dsub(1.0, c[k]), sr));
+            }
+        }
+        *(double2 *)(R.x + 2 * p[k]) = make_double2(out[0], out[1]);
+    }
 }
 
 template <int LPF, int CAP>
@@ -239,19 +279,6 @@ rf_tick_kernel(const __grid_constant__ TickBatchT<CAP> B, int64_t T, int64_t D, 
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
     const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const bool rescale = R.neg_kind != RF_NEG_NONE && R.curves[RF_CURVE_RESCALE] != nullptr;
-    if (fast_row(R, D)) {
-        for (int64_t f0 = wid * FPW; f0 < T; f0 += warps_total * FPW) {
-            const int64_t f = f0 + sub;
-            if (f >= T) continue;
-#pragma unroll
-            for (int g = 0; g < kTickMaxGroups; ++g) {
-                const int64_t c = (int64_t)g * 2 * LPF + 2 * gl;
-                if (c < D) fast_pair(R, style, f, f * D + c);
-            }
-        }
-        return;
-    }
-
     for (int64_t f0 = wid * FPW; f0 < T; f0 += warps_total * FPW) {
         const int64_t f = f0 + sub;
         const bool live = f < T;
@@ -334,6 +361,19 @@ static int launch_rows(const rf_row *rows, int n, int lpf, int64_t T, int64_t D,
     }
 }
 
+template <int CAP>
+static int launch_fast(const FastRow *rows, int n, int64_t T, int64_t D, const double *style, cudaStream_t st) {
+    FastBatchT<CAP> B;
+    B.count = n;
+    B.half_d = (uint32_t)(D / 2);
+    B.pairs = (uint32_t)(T * D / 2);
+    for (int r = 0; r < n; ++r) B.rows[r] = rows[r];
+    const unsigned bx = (B.pairs + kFastThreads * kFastPPT - 1) / (kFastThreads * kFastPPT);
+    rf_tick_fast_kernel<CAP><<<dim3(bx, (unsigned)n), kFastThreads, 0, st>>>(B, style);
+    RF_TRY_LAUNCH("rf_tick_fast_kernel");
+    return RF_OK;
+}
+
 }  // namespace rf
 
 using namespace rf;
@@ -391,12 +431,45 @@ extern "C" int rf_tick_solve(const rf_row *rows, int count, int64_t frames, int6
     int64_t half = (channels + 1) / 2;
     int lpf = 1;
     while (lpf < half && lpf < 32) lpf <<= 1;
-    for (int r0 = 0; r0 < count; r0 += kTickMaxRows) {
-        const int n = count - r0 < kTickMaxRows ? count - r0 : kTickMaxRows;
-        const int rc = n <= 4 ? launch_rows<4>(rows + r0, n, lpf, frames, channels, style_offset, st)
-                     : n <= 8 ? launch_rows<8>(rows + r0, n, lpf, frames, channels, style_offset, st)
-                              : launch_rows<kTickMaxRows>(rows + r0, n, lpf, frames, channels, style_offset, st);
-        if (rc) return rc;
+    // common rows to the lean kernel, the rest (guidance, multi-condition, ODE, morph,
+    // velocity-only) to the general one; rows are independent, so the split keeps results
+    rf_row general[kTickMaxRows];
+    FastRow fast[kTickMaxRows];
+    int ng = 0, nf = 0;
+    for (int r = 0; r <= count; ++r) {
+        if (r < count) {
+            const rf_row &R = rows[r];
+            if (fast_row(R, channels)) {
+                FastRow &F = fast[nf++];
+                F.x = R.x;
+                F.v = R.cond_x0[0];
+                F.nm = R.noise_model;
+                F.n = R.noise_step;
+                F.src = R.source;
+                F.csde = R.curves[RF_CURVE_SDE];
+                F.tc = R.t_curr;
+                F.tn = R.t_next;
+                F.jt = R.jitter_t;
+                F.flags = R.flags;
+            } else {
+                general[ng++] = R;
+            }
+        }
+        const bool last = r == count;
+        if (nf && (nf == kTickMaxRows || last)) {
+            const int rc = nf <= 4 ? launch_fast<4>(fast, nf, frames, channels, style_offset, st)
+                         : nf <= 8 ? launch_fast<8>(fast, nf, frames, channels, style_offset, st)
+                                   : launch_fast<kTickMaxRows>(fast, nf, frames, channels, style_offset, st);
+            if (rc) return rc;
+            nf = 0;
+        }
+        if (ng && (ng == kTickMaxRows || last)) {
+            const int rc = ng <= 4 ? launch_rows<4>(general, ng, lpf, frames, channels, style_offset, st)
+                         : ng <= 8 ? launch_rows<8>(general, ng, lpf, frames, channels, style_offset, st)
+                                   : launch_rows<kTickMaxRows>(general, ng, lpf, frames, channels, style_offset, st);
+            if (rc) return rc;
+            ng = 0;
+        }
     }
     return RF_OK;
 }

@@ -323,6 +323,7 @@ class StreamPipeline:
         self.launches_last_tick = 0
         self.rows_last_tick = 0
         self._phases = None  # {phase: [(start_event, end_event), ...]} when timing is on
+        self._last_solve = None
         self._views: dict = {}            # id(request) -> cached curve view (see _curve_view)
         self._views_version = -1
 
@@ -630,6 +631,7 @@ class StreamPipeline:
             self.launches_last_tick += 2
         lib = _native.load()
         arr = (RfRow * len(rows))(*rows)
+        self._last_solve = (arr, len(rows))   # kept for bench.py's per-launch solver timing
         ev = self._phase_begin("solve")
         _native.check(lib.rf_tick_solve(arr, len(rows), T, D, self.weights.device_offset.data_ptr(),
                                         self._stream.cuda_stream), "rf_tick_solve")

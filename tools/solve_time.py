@@ -1,0 +1,24 @@
+"""Device time of the config-2 toy tick's solver launch (bench.solve_launch_ms) and its HBM
+rate; run under ncu (-k regex:rf_tick) for the kernel's own duration and DRAM bytes."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2605_28657_b200 as rf  # noqa: E402
+
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+conf = rf.PipelineConfig(depth=bench.DEPTH, steps=bench.STEPS, frames=bench.T, channels=bench.D, seed=0)
+p = rf.StreamPipeline(conf, request=bench.make_request(rf, 0))
+for _ in range(32):
+    p.tick()
+torch.cuda.synchronize()
+flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+ms = bench.solve_launch_ms(p, flush, iters)
+sb = bench.DEPTH * bench.solve_bytes_per_row(True)
+hbm = bench.peaks()[0]
+print(f"solve launch {ms * 1e3:.2f} us  {sb / ms / 1e6:.1f} GB/s  frac {sb / ms / 1e6 / hbm:.3f}")
