@@ -641,12 +641,21 @@ def dit_tick_240s(rf, dit_mod, weights, rank, flush, bf16_sust, ticks=16):
     ms, done, _, ph = timed_ticks(p, ticks, flush, p.stream, phases=True)
     flops = dit_mod.DiTConfig().flops_per_forward(DEPTH, frames)
     tf = flops / (ph["model"] * 1e-3) / 1e12
+    solve_ms = solve_launch_ms(p, flush)   # last: it advances the ring
+    sb = DEPTH * frames * D * (4 * 8 + 4)  # solve_bytes_per_row(False) at T = 6000
+    hbm_peak = peaks()[0]
     del p, m
     torch.cuda.empty_cache()
     return {"workload": "config 5 generation: 240-s latent T=6000 x D=64 (3000 DiT tokens), depth 4, S=8, DiT",
             "value": round(done / (ms * 1e-3), 3), "unit": UNIT, "ms_per_step": round(ms / ticks, 3),
             "ticks": ticks, "completions": done, "phase_ms": {k: round(v, 3) for k, v in ph.items()},
-            "dit_flops_per_tick": flops, "dit_tflops": round(tf, 1), "frac_of_sustained_peak": round(tf / bf16_sust, 4)}
+            "dit_flops_per_tick": flops, "dit_tflops": round(tf, 1), "frac_of_sustained_peak": round(tf / bf16_sust, 4),
+            "solver_roofline": {"bound": "hbm", "kernel": "rf_tick_fast_kernel", "launch_us": round(solve_ms * 1e3, 2),
+                                "achieved": round(sb / (solve_ms * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
+                                "frac": round(sb / (solve_ms * 1e-3) / 1e9 / hbm_peak, 4),
+                                "algorithmic_bytes_per_launch": sb,
+                                "note": "DiT rows: x read + write, source, SDE noise (f64), velocity (f32); "
+                                        "bench.solve_launch_ms"}}
 
 
 def run_stub(args):

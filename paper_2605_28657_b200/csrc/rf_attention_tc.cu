@@ -454,7 +454,17 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
     const uint32_t tmem = *tmem_slot;
     pdl_wait();
     pdl_launch();
-    if (tid == 0) FA_GTRACE(0);
+    if (tid == 0) {
+        FA_GTRACE(0);
+        // NH = 1 leaves event row 3 free: SM id, entry and exit clocks (tools/attn_trace.py)
+        if (trace_buf) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            unsigned long long *r3 = trace_buf + ((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 3) * 16;
+            r3[15] = smid;
+            r3[14] = clock64();
+        }
+    }
 
     if (warp == TMA_WARP) {
         if (elect_one()) {
@@ -640,7 +650,10 @@ rf_attn_fa64_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constan
     }
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) FA_GTRACE(1);
+    if (tid == 0) {
+        FA_GTRACE(1);
+        if (trace_buf) trace_buf[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 3) * 16 + 13] = clock64();
+    }
     if (warp == MMA_WARP) tmem_dealloc<256 * NH>(tmem);
 }
 

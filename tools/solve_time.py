@@ -12,7 +12,9 @@ import bench  # noqa: E402
 import paper_2605_28657_b200 as rf  # noqa: E402
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-conf = rf.PipelineConfig(depth=bench.DEPTH, steps=bench.STEPS, frames=bench.T, channels=bench.D, seed=0)
+frames = int(sys.argv[2]) if len(sys.argv) > 2 else bench.T
+bench.T = frames
+conf = rf.PipelineConfig(depth=bench.DEPTH, steps=bench.STEPS, frames=frames, channels=bench.D, seed=0)
 p = rf.StreamPipeline(conf, request=bench.make_request(rf, 0))
 for _ in range(32):
     p.tick()
@@ -21,4 +23,4 @@ flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda
 ms = bench.solve_launch_ms(p, flush, iters)
 sb = bench.DEPTH * bench.solve_bytes_per_row(True)
 hbm = bench.peaks()[0]
-print(f"solve launch {ms * 1e3:.2f} us  {sb / ms / 1e6:.1f} GB/s  frac {sb / ms / 1e6 / hbm:.3f}")
+print(f"T={frames}: solve launch {ms * 1e3:.2f} us  {sb / ms / 1e6:.1f} GB/s  frac {sb / ms / 1e6 / hbm:.3f}")
