@@ -261,10 +261,15 @@ def timed_ticks(pipe, steps, flush, stream, phases=False):
 
 def solve_launch_ms(pipe, flush, iters=40):
     """Device time of the tick's solver launch alone: the last tick's rows re-launched
-    through rf_tick_solve, L2 flushed before each (outside the events), CUDA events on the
-    pipeline stream.  The in-tick phase events also hold the host's launch gap when the GPU
-    waits for the Python tick (the toy path); the flush queued ahead keeps the stream busy
-    here, so the events bracket the kernel alone.  Advances the ring state (timing only)."""
+    through rf_tick_solve, CUDA events on the pipeline stream, inputs evicted from L2 before
+    each launch (outside the events).  The in-tick phase events also hold the host's launch
+    gap when the GPU waits for the Python tick (the toy path); the flush queued ahead keeps
+    the stream busy here, so the events bracket the kernel alone.  Two evictions, both
+    timed: "dirty" = the bench's 256-MiB write flush alone (L2 left full of dirty lines the
+    solver's reads must write back first: +50-100% at these sizes), "clean" = the write flush
+    then a read of the same buffer (the dirty lines written back outside the events; L2 holds
+    only clean flush lines, none of the solver's inputs -- ncu's --cache-control all state).
+    Returns (clean_ms, dirty_ms).  Advances the ring state (timing only)."""
     import torch
 
     from paper_2605_28657_b200 import _native
@@ -273,18 +278,23 @@ def solve_launch_ms(pipe, flush, iters=40):
     lib = _native.load()
     T_, D_ = pipe.config.shape
     st = pipe.stream
-    ts = []
-    for _ in range(iters):
-        with torch.cuda.stream(st):
-            flush.fill_(1)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        _native.check(lib.rf_tick_solve(arr, n, T_, D_, pipe.weights.device_offset.data_ptr(), st.cuda_stream),
-                      "rf_tick_solve")
-        b.record(st)
-        ts.append((a, b))
-    torch.cuda.synchronize()
-    return sum(a.elapsed_time(b) for a, b in ts) / iters
+    res = []
+    for clean in (True, False):
+        ts = []
+        for _ in range(iters):
+            with torch.cuda.stream(st):
+                flush.fill_(1)
+                if clean:
+                    torch.amax(flush)   # reads every flush line back (no dirty lines left)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            _native.check(lib.rf_tick_solve(arr, n, T_, D_, pipe.weights.device_offset.data_ptr(), st.cuda_stream),
+                          "rf_tick_solve")
+            b.record(st)
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        res.append(sum(a.elapsed_time(b) for a, b in ts) / iters)
+    return res[0], res[1]
 
 
 def decode_240s(codec, world, rank, flush, hbm_peak, iters=10):
@@ -530,7 +540,7 @@ def run_ours(args):
         w_s = time.perf_counter() - w0
         nc = tp.noise_cache
         cache_stats = {"hits": nc.hits, "misses": nc.misses, "resident_bytes": nc.bytes}
-        solve_ms = solve_launch_ms(tp, flush)   # last: it advances the ring
+        solve_ms, solve_dirty_ms = solve_launch_ms(tp, flush)   # last: it advances the ring
         del tp
         # the same leg with the noise cache off (every draw regenerated every tick)
         tq = rf.StreamPipeline(conf, request=make_request(rf, rank), noise_cache_bytes=0)
@@ -550,10 +560,13 @@ def run_ours(args):
                                    "achieved": round(sb / (solve_ms * 1e-3) / 1e9, 1), "peak": hbm_peak,
                                    "unit": "GB/s", "frac": round(sb / (solve_ms * 1e-3) / 1e9 / hbm_peak, 4),
                                    "launch_us": round(solve_ms * 1e3, 2),
+                                   "launch_us_behind_dirty_flush": round(solve_dirty_ms * 1e3, 2),
                                    "algorithmic_bytes_per_launch": sb,
-                                   "note": "the tick's solver launch re-issued 40x behind an L2 flush, CUDA events "
-                                           "on the pipeline stream (bench.solve_launch_ms); phase_ms.solve also "
-                                           "holds the host's launch gap"},
+                                   "note": "the tick's solver launch re-issued 40x with its inputs evicted from L2 "
+                                           "(write flush + read-back: clean L2, as ncu's cache control), CUDA events "
+                                           "on the pipeline stream (bench.solve_launch_ms); behind the write flush "
+                                           "alone the solver first writes back ~126 MB of dirty flush lines; "
+                                           "phase_ms.solve also holds the host's launch gap"},
                "gpu_launches": t_launch, "dtype": "f64",
                "note": "same ring and solver with ToyFlowModel velocities (bit-exact vs the reference)"}
 
@@ -641,7 +654,7 @@ def dit_tick_240s(rf, dit_mod, weights, rank, flush, bf16_sust, ticks=16):
     ms, done, _, ph = timed_ticks(p, ticks, flush, p.stream, phases=True)
     flops = dit_mod.DiTConfig().flops_per_forward(DEPTH, frames)
     tf = flops / (ph["model"] * 1e-3) / 1e12
-    solve_ms = solve_launch_ms(p, flush)   # last: it advances the ring
+    solve_ms, solve_dirty_ms = solve_launch_ms(p, flush)   # last: it advances the ring
     sb = DEPTH * frames * D * (4 * 8 + 4)  # solve_bytes_per_row(False) at T = 6000
     hbm_peak = peaks()[0]
     del p, m
@@ -651,6 +664,7 @@ def dit_tick_240s(rf, dit_mod, weights, rank, flush, bf16_sust, ticks=16):
             "ticks": ticks, "completions": done, "phase_ms": {k: round(v, 3) for k, v in ph.items()},
             "dit_flops_per_tick": flops, "dit_tflops": round(tf, 1), "frac_of_sustained_peak": round(tf / bf16_sust, 4),
             "solver_roofline": {"bound": "hbm", "kernel": "rf_tick_fast_kernel", "launch_us": round(solve_ms * 1e3, 2),
+                                "launch_us_behind_dirty_flush": round(solve_dirty_ms * 1e3, 2),
                                 "achieved": round(sb / (solve_ms * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
                                 "frac": round(sb / (solve_ms * 1e-3) / 1e9 / hbm_peak, 4),
                                 "algorithmic_bytes_per_launch": sb,

@@ -157,3 +157,17 @@ def test_backpressure_and_errors(rf):
         pipe.set_shared_curve("nope", 1.0)
     with pytest.raises(ValueError):
         pipe.set_mode("nope")
+
+
+def test_deep_ring_mixed_rows_bit_exact(rf):
+    """More active rows than one solver launch takes (40 > 32), common SDE rows and
+    morphing rows in the same tick: the host splits them between the lean and the general
+    solver kernels, in chunks; every byte matches the oracle."""
+    spec = dict(config=dict(depth=40, steps=8), request=dict(prompt="p", source="src", hint=1.0),
+                ops=[("tick", 48), ("set_shared_curve", "x0_target", "target"), ("tick", 12)])
+    gpu = scenarios.drive(rf, spec)
+    cpu = scenarios.drive_oracle(spec)
+    for k in scenarios.EXACT_FIELDS:
+        assert np.array_equal(gpu[k], cpu[k]), k
+    assert len(gpu["latents"]) > 40
+    assert np.array_equal(np.array([sha(x) for x in gpu["latents"]]), np.array([sha(x) for x in cpu["latents"]]))
