@@ -19,6 +19,8 @@ struct AdmitBatch {
 
 // _admit (pipeline.py:523-532): x = noise, or d*noise + (1-d)*source.
 __global__ void rf_admit_kernel(const __grid_constant__ AdmitBatch B, int64_t numel) {
+    pdl_wait();
+    pdl_launch();
     const rf_admit &A = B.a[blockIdx.y];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -71,6 +73,8 @@ rf_emit_partials(const __grid_constant__ EmitBatch B, int64_t numel, const doubl
                  double *__restrict__ mse_prev, double *__restrict__ mse_ref, int has_last) {
     __shared__ double sh[kRedThreads / 32];
     __shared__ bool last_block;
+    pdl_wait();
+    pdl_launch();
     const int e = blockIdx.y;
     const double *lat = B.e[e].latent;
     double *rec = B.e[e].record;
@@ -152,7 +156,7 @@ extern "C" int rf_admit_init(const rf_admit *admits, int count, int64_t numel, v
         }
         int64_t bx = (numel + 255) / 256;
         if (bx > 1024) bx = 1024;
-        rf_admit_kernel<<<dim3((unsigned)bx, (unsigned)B.count), 256, 0, st>>>(B, numel);
+        RF_TRY_CUDA(launch_pdl(rf_admit_kernel, dim3((unsigned)bx, (unsigned)B.count), dim3(256), 0, st, B, numel));
         RF_TRY_LAUNCH("rf_admit_kernel");
     }
     return RF_OK;
@@ -224,8 +228,9 @@ extern "C" int rf_emit_stats(const rf_emit *emits, int count, int64_t numel, con
             }
         }
         const double *prev = c0 == 0 ? last : emits[c0 - 1].latent;
-        rf_emit_partials<<<dim3((unsigned)chunks, (unsigned)B.count), kRedThreads, 0, st>>>(
-            B, numel, prev, reference, pp, pr, status, done, mse_prev + c0, mse_ref + c0, prev != nullptr);
+        RF_TRY_CUDA(launch_pdl(rf_emit_partials, dim3((unsigned)chunks, (unsigned)B.count), dim3(kRedThreads), 0, st,
+                               B, numel, prev, reference, pp, pr, status, done, mse_prev + c0, mse_ref + c0,
+                               (int)(prev != nullptr)));
         RF_TRY_LAUNCH("rf_emit_partials");
     }
     return RF_OK;

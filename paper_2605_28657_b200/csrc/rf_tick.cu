@@ -211,6 +211,8 @@ constexpr int kFastMinBlocks = 4;
 template <int CAP>
 __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks)
 rf_tick_fast_kernel(const __grid_constant__ FastBatchT<CAP> B, const double *__restrict__ style) {
+    pdl_wait();     // programmatic dependent launch: the prologue overlaps the previous kernel's tail
+    pdl_launch();
     const FastRow &R = B.rows[blockIdx.y];
     const bool cond_v = (R.flags & RF_ROWF_COND_V) != 0, v32 = (R.flags & RF_ROWF_V_F32) != 0;
     const bool sty = !cond_v || (R.flags & RF_ROWF_STYLE_V);
@@ -272,6 +274,8 @@ rf_tick_fast_kernel(const __grid_constant__ FastBatchT<CAP> B, const double *__r
 template <int LPF, int CAP>
 __global__ void __launch_bounds__(256)
 rf_tick_kernel(const __grid_constant__ TickBatchT<CAP> B, int64_t T, int64_t D, const double *__restrict__ style) {
+    pdl_wait();
+    pdl_launch();
     const rf_row &R = B.rows[blockIdx.y];
     const int lane = threadIdx.x & 31;
     constexpr int FPW = 32 / LPF;  // frames per warp step
@@ -340,7 +344,7 @@ static int launch_tick(const TickBatchT<CAP> &B, int64_t T, int64_t D, const dou
     // keep >= ~2 waves over the SMs across all rows without oversubscribing tiny rows
     if (bx < 1) bx = 1;
     dim3 grid((unsigned)bx, (unsigned)B.count);
-    rf_tick_kernel<LPF, CAP><<<grid, warps_per_block * 32, 0, st>>>(B, T, D, style);
+    RF_TRY_CUDA(launch_pdl(rf_tick_kernel<LPF, CAP>, grid, dim3(warps_per_block * 32), 0, st, B, T, D, style));
     RF_TRY_LAUNCH("rf_tick_kernel");
     return RF_OK;
 }
@@ -369,7 +373,7 @@ static int launch_fast(const FastRow *rows, int n, int64_t T, int64_t D, const d
     B.pairs = (uint32_t)(T * D / 2);
     for (int r = 0; r < n; ++r) B.rows[r] = rows[r];
     const unsigned bx = (B.pairs + kFastThreads * kFastPPT - 1) / (kFastThreads * kFastPPT);
-    rf_tick_fast_kernel<CAP><<<dim3(bx, (unsigned)n), kFastThreads, 0, st>>>(B, style);
+    RF_TRY_CUDA(launch_pdl(rf_tick_fast_kernel<CAP>, dim3(bx, (unsigned)n), dim3(kFastThreads), 0, st, B, style));
     RF_TRY_LAUNCH("rf_tick_fast_kernel");
     return RF_OK;
 }
