@@ -385,10 +385,14 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     // The set-aside is device-wide state: the first live DiT saves the previous limit and the
     // last one destroyed restores it (other work on the device gets its L2 back).
     {
-        int dev = 0, maxp = 0;
-        const size_t hb = (size_t)max_rows * d->tokens * c.d_model * sizeof(float);
+        int dev = 0, maxp = 0, maxw = 0;
+        size_t hb = (size_t)max_rows * d->tokens * c.d_model * sizeof(float);
         if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < kMaxDevices &&
-            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && maxp > 0) {
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && maxp > 0 &&
+            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess && maxw > 0) {
+            // a window larger than the device maximum makes every launch that carries it fail
+            // (cudaErrorInvalidValue): long latents x many rows cover the leading rows only
+            if (hb > (size_t)maxw) hb = (size_t)maxw;
             std::lock_guard<std::mutex> g(g_l2_mu);
             size_t lim = hb < (size_t)maxp ? hb : (size_t)maxp, cur = 0;
             if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess) {

@@ -284,3 +284,18 @@ def _persisting_limit() -> int:
     err, v = cudart.cudaDeviceGetLimit(cudart.cudaLimit.cudaLimitPersistingL2CacheSize)
     assert int(err) == 0, err
     return int(v)
+
+
+def test_residual_stream_larger_than_the_l2_window(dit_mod):
+    """max_rows x tokens x d_model x 4 B above the device's maximum access-policy window
+    (here 32 x 10 000 x 256 x 4 = 328 MB): the persisting window is clamped, the forward
+    runs, and a row's velocity is bit-identical to the same row in a small-capacity DiT."""
+    cfg = dit_mod.DiTConfig().small()
+    w = dit_mod.DiTWeights(cfg)
+    big = dit_mod.DiT(cfg, frames=20000, max_rows=32, weights=w)
+    one = dit_mod.DiT(cfg, frames=20000, max_rows=1, weights=w)
+    xs, ts, conds = _inputs(big, 2, 20000, 64, seed=9)
+    a = big.forward(xs, ts, conds).clone()
+    b = one.forward(xs[1:], ts[1:], conds[1:]).clone()
+    assert torch.isfinite(a).all()
+    assert torch.equal(a[1], b[0])

@@ -13,10 +13,11 @@ def main():
     # a non-default stream, so the forward runs as its captured CUDA graph
     torch.cuda.set_stream(torch.cuda.Stream())
     rows = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    frames = next((int(a.split("=")[1]) for a in sys.argv if a.startswith("--frames=")), 1500)
     cfg = D.DiTConfig()
-    dit = D.DiT(cfg, frames=1500, max_rows=max(rows, 8))
+    dit = D.DiT(cfg, frames=frames, max_rows=max(rows, 8))
     g = torch.Generator(device="cuda").manual_seed(0)
-    xs = [torch.randn(1500, 64, device="cuda", generator=g, dtype=torch.float64) for _ in range(rows)]
+    xs = [torch.randn(frames, 64, device="cuda", generator=g, dtype=torch.float64) for _ in range(rows)]
     ts = [1.0 - 0.1 * i for i in range(rows)]
     conds = [dit.cond_tokens(i) for i in range(rows)]
     out = dit.forward(xs, ts, conds).clone()
@@ -35,7 +36,7 @@ def main():
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / n
-    fl = cfg.flops_per_forward(rows, 1500)
+    fl = cfg.flops_per_forward(rows, frames)
     print(f"forward {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s  ({fl / 1e12:.2f} TFLOP)  params={cfg.params() / 1e9:.2f}B")
     if "--graph" in sys.argv:   # same forward replayed from a CUDA graph (no host launch gaps)
         s = torch.cuda.Stream()
