@@ -55,8 +55,8 @@ struct EpiArgs {
     // RMSNorm fused across a GEMM boundary (the norm without modulation before the
     // cross-attention query projection):
     //  kResidGate (TMA-staged): with aux set, also aux[m * aux_ld + n] = bf16 of the
-    //    updated residual and sq_part[(n / BN) * sq_ld + m] = its sum of squares over the
-    //    tile's BN columns (ascending column order);
+    //    updated residual and sq_part[(n / 128) * sq_ld + m] = its sum of squares over
+    //    each 128 columns (ascending column order, whatever BN);
     //  kStoreBF16: with rs_part set, acc is scaled by rsqrt(sum_t rs_part[t * rs_ld + m] *
     //    rs_inv_d + rs_eps) (t ascending) before rounding -- the consumer applies the norm.
     __nv_bfloat16 *aux;
@@ -386,6 +386,12 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                         for (int v = 0; v < 4; ++v)
                             pk[v] = make_uint4(aux4[2 * v].x, aux4[2 * v].y, aux4[2 * v + 1].x, aux4[2 * v + 1].y);
                         store_rows_bf16x32(epi.aux, epi.aux_ld, m0, M, n0 + col, lane, pk);
+                        // one partial sum of squares per 128 columns whatever the tile width, so
+                        // the consumer's sum (and the row's result) does not depend on BN
+                        if ((col + 32) % 128 == 0) {
+                            if (live) epi.sq_part[(int64_t)((n0 + col) / 128) * epi.sq_ld + m0 + lane] = ss;
+                            ss = 0.f;
+                        }
                     }
                 }
                 if (p == NP - 1) tc_fence_before();
@@ -412,7 +418,6 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                     }
                 }
             }
-            if (epi.aux && live) epi.sq_part[(int64_t)(n0 / BN) * epi.sq_ld + m0 + lane] = ss;
             }
             if (++acc == 2) {
                 acc = 0;

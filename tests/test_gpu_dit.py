@@ -299,3 +299,17 @@ def test_residual_stream_larger_than_the_l2_window(dit_mod):
     b = one.forward(xs[1:], ts[1:], conds[1:]).clone()
     assert torch.isfinite(a).all()
     assert torch.equal(a[1], b[0])
+
+
+@pytest.mark.parametrize("rows", [2, 3, 8])
+def test_row_bit_identical_across_projection_tile_widths(dit_mod, rows):
+    """The O / cross-O / down projections take 256 x 256 tiles in forwards with enough rows
+    (8 rows at T = 1500) and 256 x 128 tiles in small ones (1 row): a row's velocity is the
+    same bytes either way (same per-element MMA reduction; the fused norm's partial sums are
+    per 128 columns whatever the tile width)."""
+    dit = dit_mod.DiT(dit_mod.DiTConfig(), frames=1500, max_rows=8)
+    xs, ts, conds = _inputs(dit, rows, 1500, 64, seed=11)
+    full = dit.forward(xs, ts, conds).clone()
+    for r in (0, rows - 1):
+        one = dit.forward(xs[r:r + 1], ts[r:r + 1], conds[r:r + 1]).clone()
+        assert torch.equal(full[r], one[0]), r
