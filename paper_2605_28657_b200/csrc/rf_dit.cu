@@ -202,8 +202,10 @@ struct Dit {
     // GEMM plans (tensor maps at max rows)
     GemmPlan p_in, p_t1, p_t2, p_ada, p_fada, p_out, p_kvc;
     std::vector<GemmPlan> p_qkv, p_o, p_qc, p_oc, p_gu, p_down;
-    // the d_model-wide projections (O, cross-O, down) with 256 x 256 pair tiles (proj_wide)
-    std::vector<GemmPlan> p_o_w, p_oc_w, p_down_w;
+    // The N = d_model projections (O, cross-O, down) with 256 x 256 pair tiles, for forwards
+    // whose row count makes them pay (proj_wide); [O, cross-O, down][layer], built on first use
+    std::vector<GemmPlan> proj_wide_plans[3];
+    bool proj_wide_ok = false, proj_built = false;
     int proj_pairs = 74;   // CTA pairs on the device
 };
 
@@ -348,15 +350,14 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     d->p_oc.resize(L);
     d->p_gu.resize(L);
     d->p_down.resize(L);
-    // The N = d_model projections (O, cross-O, down) get 256 x 128 or 256 x 256 pair tiles
-    // per forward, by its row count (proj_wide): a 256 x 128 tile is operand-feed-bound at
-    // ~0.6 of a 256 x 256 tile's time (not 0.5), and 256-wide tiles quantise worse at small
-    // M -- config 2 (12 m-tiles: 2 waves of 96 wide vs 3 of 192 narrow) stays narrow (wide
-    // measured 3-4% slower), config 3's 8 rows and config 5's 3000-token rows go wide (6% and
-    // 7-9% faster forwards; tools/dit_check.py A/B, profiles/r2_proj_tiles.txt).  Both tile
-    // widths give bit-identical rows (the same per-element MMA reduction; the fused norm's
-    // partial sums are per 128 columns either way), so a row's velocity still does not depend
-    // on the batch it rides in.
+    // The N = d_model projections (O, cross-O, down): a 256 x 128 pair tile is operand-feed-
+    // bound at ~0.6 of a 256 x 256 tile's time (not 0.5), while 256-wide tiles quantise worse.
+    // Per forward (proj_wide, by its row count): config 2 (12 m-tiles: three waves of 192
+    // narrow tiles vs two of 96 wide) stays narrow -- all wide measured 3-4% slower; config
+    // 3's 8 rows and config 5's 3000-token rows go wide (5-7% faster forwards).  Both give
+    // bit-identical rows (the same per-element MMA reduction; the fused norm's partial sums
+    // are per 128 columns), so a row's velocity does not depend on its batch
+    // (tools/dit_check.py A/B, profiles/r2_proj_tiles.txt).
     {
         int dev = 0, sms = 0;
         if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -364,11 +365,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
             sms = 148;
         cudaGetLastError();
         d->proj_pairs = sms / 2;
-        if (D % 256 == 0 && D >= 512 && BN >= pair_min_m) {
-            d->p_o_w.resize(L);
-            d->p_oc_w.resize(L);
-            d->p_down_w.resize(L);
-        }
+        d->proj_wide_ok = D % 256 == 0 && D >= 512 && BN >= pair_min_m;
     }
     const __nv_bfloat16 *wq = (const __nv_bfloat16 *)w->w_qkv, *wo = (const __nv_bfloat16 *)w->w_o;
     const __nv_bfloat16 *wqc = (const __nv_bfloat16 *)w->w_qc, *wkvc = (const __nv_bfloat16 *)w->w_kvc;
@@ -385,15 +382,6 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         // gated-residual outputs all update h: bind it once (TMA map of the epilogue)
         for (GemmPlan *g : {&d->p_o[l], &d->p_oc[l], &d->p_down[l]})
             if (!rc) rc = gemm_plan_c(g, d->h, D);
-        if (!d->p_o_w.empty()) {
-            auto wide = [&](GemmPlan *p, const void *A, const void *Bw, int64_t K) {
-                if (!rc) rc = gemm_plan(p, A, Bw, BN, D, K, K, K, 256, 2);
-                if (!rc) rc = gemm_plan_c(p, d->h, D);
-            };
-            wide(&d->p_o_w[l], d->att, wo + l * D * d->q_dim, d->q_dim);
-            wide(&d->p_oc_w[l], d->att, woc + l * D * d->q_dim, d->q_dim);
-            wide(&d->p_down_w[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, c.mlp_hidden);
-        }
         if (!rc && d->p_gu[l].bn == 256) rc = gemm_plan_o(&d->p_gu[l], d->mlp, c.mlp_hidden);
     }
     // the cross-attention K/V projections of all layers read the same conditioning tokens:
@@ -503,13 +491,38 @@ static int dit_body(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
     g_l2_window = L2Window{};
     return rc;
 }
-// 256 x 256 tiles for the N = d_model projections of an M-row forward: waves of wide tiles
-// vs waves of 256 x 128 tiles at 0.6 of their time each (see rf_dit_create)
+// Tiles of the N = d_model projections for an M-row forward: false = 256 x 128 pair tiles
+// (p_o / p_oc / p_down), true = 256 x 256 (proj_wide_*), by the waves each needs on the CTA
+// pairs (a narrow tile takes ~0.6 of a wide tile's time).  A column split (wide tiles for the
+// first columns, narrow for the rest, two launches) measured slower than either pure form
+// (config 2 with 6 + 2 wide-column tiles: +1.5% forward; config 5: +4% vs all wide;
+// profiles/r2_proj_tiles.txt).
 static bool proj_wide(const Dit &d, int64_t M) {
-    if (d.p_o_w.empty()) return false;
-    const int64_t mt = (M + 255) / 256, D = d.c.d_model, P = d.proj_pairs;
-    const int64_t waves_w = (mt * (D / 256) + P - 1) / P, waves_n = (mt * (D / 128) + P - 1) / P;
-    return 5 * waves_w < 3 * waves_n;
+    if (!d.proj_wide_ok) return false;
+    const int64_t mt = (M + 255) / 256, n = d.c.d_model / 256, P = d.proj_pairs;
+    auto waves = [&](int64_t tiles) { return (tiles + P - 1) / P; };
+    return 5 * waves(mt * n) < 3 * waves(mt * 2 * n);
+}
+
+// the 256 x 256 plans, built on the first forward that uses them
+static int proj_build(Dit &d) {
+    if (d.proj_built) return RF_OK;
+    const rf_dit_config &c = d.c;
+    const int64_t D = c.d_model, L = c.n_layers, BN = (int64_t)d.max_rows * d.tokens;
+    const __nv_bfloat16 *wts[3] = {(const __nv_bfloat16 *)d.w.w_o, (const __nv_bfloat16 *)d.w.w_oc,
+                                   (const __nv_bfloat16 *)d.w.w_down};
+    const void *act[3] = {d.att, d.att, d.mlp};
+    const int64_t kdim[3] = {d.q_dim, d.q_dim, c.mlp_hidden};
+    for (int g = 0; g < 3; ++g) {
+        d.proj_wide_plans[g].resize(L);
+        for (int64_t l = 0; l < L; ++l) {
+            GemmPlan &p = d.proj_wide_plans[g][l];
+            RF_TRY(gemm_plan(&p, act[g], wts[g] + l * D * kdim[g], BN, D, kdim[g], kdim[g], kdim[g], 256, 2));
+            RF_TRY(gemm_plan_c(&p, d.h, D));
+        }
+    }
+    d.proj_built = true;
+    return RF_OK;
 }
 
 static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) {
@@ -543,10 +556,14 @@ static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) 
     // h = in_proj(patches)
     RF_TRY(gemm_run(d.p_in, RF_EPI_F32, d.h, D, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
     const bool wide = proj_wide(d, M);
+    // gated-residual projection g (0 O, 1 cross-O, 2 down) of layer l
+    auto proj = [&](int g, int64_t l, const float *gate, int64_t gate_ld, const NormFuse *nf) -> int {
+        const GemmPlan *narrow[3] = {&d.p_o[l], &d.p_oc[l], &d.p_down[l]};
+        return gemm_run(wide ? d.proj_wide_plans[g][l] : *narrow[g], RF_EPI_RESID_GATE, d.h, D, gate, gate_ld, (int)N,
+                        1.f, st, nullptr, 0, M, nullptr, nf);
+    };
     for (int64_t l = 0; l < L; ++l) {
         const float *md = d.mods + l * B * W6;  // [B][6][D]: shift,scale,gate (msa), shift,scale,gate (mlp)
-        const GemmPlan &po = wide ? d.p_o_w[l] : d.p_o[l], &poc = wide ? d.p_oc_w[l] : d.p_oc[l];
-        const GemmPlan &pdn = wide ? d.p_down_w[l] : d.p_down[l];
         // self-attention
         RF_TRY(norm_mod(d, d.h, M, md + 0 * D, md + 1 * D, W6, d.a, st));
         const VtOut vts{d.vt_self, (int)(d.q_dim + d.kv_dim), c.n_kv_heads, d.n_pad};
@@ -566,8 +583,7 @@ static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) 
             nf_in.rs_inv_d = 1.0f / (float)D;
             nf_in.rs_eps = c.norm_eps;
         }
-        RF_TRY(gemm_run(po, RF_EPI_RESID_GATE, d.h, D, md + 2 * D, W6, (int)N, 1.f, st, nullptr, 0, M,
-                        nullptr, d.fuse_norm2 ? &nf_out : nullptr));
+        RF_TRY(proj(0, l, md + 2 * D, W6, d.fuse_norm2 ? &nf_out : nullptr));
         // cross-attention to the row's conditioning tokens (residual, no gate)
         if (!d.fuse_norm2) RF_TRY(norm_mod(d, d.h, M, nullptr, nullptr, 0, d.a, st));
         const bool xattn = d.fuse_xattn;
@@ -581,11 +597,11 @@ static int dit_body_(const Dit &d, int32_t rows, float *v_out, cudaStream_t st) 
                             d.fuse_norm2 ? &nf_in : nullptr));
             RF_TRY(attn_run(d.a_cross[l], d.att, d.q_dim, (int)B, st));
         }
-        RF_TRY(gemm_run(poc, RF_EPI_RESID_GATE, d.h, D, d.w.ones, 0, (int)N, 1.f, st, nullptr, 0, M));
+        RF_TRY(proj(1, l, d.w.ones, 0, nullptr));
         // SwiGLU MLP
         RF_TRY(norm_mod(d, d.h, M, md + 3 * D, md + 4 * D, W6, d.a, st));
         RF_TRY(gemm_run(d.p_gu[l], RF_EPI_SWIGLU, d.mlp, c.mlp_hidden, nullptr, 0, 1, 1.f, st, nullptr, 0, M));
-        RF_TRY(gemm_run(pdn, RF_EPI_RESID_GATE, d.h, D, md + 5 * D, W6, (int)N, 1.f, st, nullptr, 0, M));
+        RF_TRY(proj(2, l, md + 5 * D, W6, nullptr));
     }
     // final AdaLN + output projection (fp32), tokens [B, N, p*C] == latent [B, T, C]
     RF_TRY(norm_mod(d, d.h, M, d.fmod, d.fmod + D, 2 * D, d.a, st));
@@ -602,6 +618,7 @@ extern "C" int rf_dit_forward(void *handle, int32_t rows, const double *const *x
     }
     Dit &d = *dp;
     cudaStream_t st = (cudaStream_t)stream;
+    if (proj_wide(d, (int64_t)rows * d.tokens)) RF_TRY(proj_build(d));
     RowPtrs R{};
     for (int b = 0; b < rows; ++b) {
         R.x[b] = x_rows[b];

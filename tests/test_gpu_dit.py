@@ -301,12 +301,12 @@ def test_residual_stream_larger_than_the_l2_window(dit_mod):
     assert torch.equal(a[1], b[0])
 
 
-@pytest.mark.parametrize("rows", [2, 3, 8])
+@pytest.mark.parametrize("rows", [2, 3, 4, 5, 8])
 def test_row_bit_identical_across_projection_tile_widths(dit_mod, rows):
-    """The O / cross-O / down projections take 256 x 256 tiles in forwards with enough rows
-    (8 rows at T = 1500) and 256 x 128 tiles in small ones (1 row): a row's velocity is the
-    same bytes either way (same per-element MMA reduction; the fused norm's partial sums are
-    per 128 columns whatever the tile width)."""
+    """The O / cross-O / down projections take 256 x 256 or 256 x 128 tiles by the forward's
+    row count (256 x 128 at 1 and 4 rows, 256 x 256 at 2, 3, 5 and 8): a row's velocity is
+    the same bytes either way (same per-element MMA reduction; the fused norm's partial sums
+    are per 128 columns whatever the tile width)."""
     dit = dit_mod.DiT(dit_mod.DiTConfig(), frames=1500, max_rows=8)
     xs, ts, conds = _inputs(dit, rows, 1500, 64, seed=11)
     full = dit.forward(xs, ts, conds).clone()
