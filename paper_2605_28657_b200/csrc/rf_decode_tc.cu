@@ -28,7 +28,7 @@
 // hi/lo split) writes the next layer's operand in place.
 //
 // Upsampler.  pcm[f][j] = quantize(sum_c h[f][c] U[j][c]): the hop columns are cut into
-// chunks of cw <= 240 (N of the MMA); a CTA owns a slice of the chunks of its tile (the
+// chunks of cw <= 128 (N of the MMA); a CTA owns a slice of the chunks of its tile (the
 // grid is tiles x slices, sized to the SM count), double-buffers them in TMEM (2 x 256
 // columns) so the quantize epilogue of chunk c overlaps the MMAs of chunk c+1, and writes
 // each row's int16 piece with a bulk (TMA) store from shared memory.
@@ -50,7 +50,9 @@ using namespace ::rf::sm100;
 constexpr int kRows = 128;           // M of every MMA
 constexpr int kPad = 16;             // zero rows above / below the tile (max dilation)
 constexpr int kBufRows = kRows + 2 * kPad;
-constexpr int kMaxCW = 240;          // upsampler chunk width (N)
+// upsampler chunk width (N): 128 -- hop 1920 in 15 chunks, one per CTA of a 3-s window
+// (was 240: 8 chunks; the window's upsampler phase 3.4 -> 2.5 us, tools/decode_trace.py)
+constexpr int kMaxCW = 128;
 constexpr int kEpiWarps = 16;         // 4 column groups x 4 lane quarters
 constexpr int kGroups = kEpiWarps / 4;
 constexpr int kThreads = (kEpiWarps + 2) * 32;

@@ -29,13 +29,16 @@ for _ in range(100):
 b.record()
 torch.cuda.synchronize()
 print(f"back-to-back: {a.elapsed_time(b) / 100 * 1e3:.2f} us per window")
-for label, busy in (("behind flush", True), ("idle stream", False)):
+for label, mode in (("behind flush (dirty L2)", "dirty"), ("behind flush + read-back (clean L2)", "clean"),
+                    ("idle stream", "idle")):
     res = []
     for _ in range(20):
-        if busy:
-            flush.fill_(1)
-        else:
+        if mode == "idle":
             torch.cuda.synchronize()
+        else:
+            flush.fill_(1)
+            if mode == "clean":
+                torch.amax(flush)
         a, b = E(), E()
         a.record()
         codec.decode_device(lat, T - W, T, OV, False, out=out)
