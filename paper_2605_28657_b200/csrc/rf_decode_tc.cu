@@ -243,6 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1) rf_decode_tc_kernel(const __grid_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // programmatic dependent launch: the barrier / TMEM setup above overlaps the previous
+    // kernel's tail; the latent and the weights are read only after it has completed
+    pdl_wait();
+    pdl_launch();
     if (threadIdx.x == 0) dtrace(A, 1);
 
     if (warp == kEpiWarps) {
@@ -637,7 +641,7 @@ extern "C" int rf_decode_window_tc(const double *latent, int64_t frames, int64_t
     const uint32_t smem = g.CP == 16 ? Smem<16>::TOTAL : g.CP == 32 ? Smem<32>::TOTAL
                         : g.CP == 48 ? Smem<48>::TOTAL : Smem<64>::TOTAL;
     RF_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)(tiles * slices), kThreads, smem, (cudaStream_t)stream>>>(A);
+    RF_TRY_CUDA(launch_pdl(kern, dim3((unsigned)(tiles * slices)), dim3(kThreads), smem, (cudaStream_t)stream, A));
     RF_TRY_LAUNCH("rf_decode_tc_kernel");
     return RF_OK;
 }
