@@ -101,7 +101,8 @@ constexpr size_t fa_smem() {
     return 1024 + (size_t)(NH + 2 * KVS) * kOperand + 256;
 }
 
-// debugging timeline ([cta][16 events][16] u64 clock64), set by rf_attn_set_trace; null in production
+// debugging timeline ([cta][16 events][16] u64: clock64 per key tile j < 15, globaltimer / SM id in the
+// last slots), set by rf_attn_set_trace; null in production
 __device__ unsigned long long *g_attn_trace = nullptr;
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -115,7 +116,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     } while (0)
 #define FA_TRACE(ev, j)                                                                                  \
     do {                                                                                                 \
-        if (trace_buf && (j) < 16)                                                                       \
+        if (trace_buf && (j) < 15)                                                                       \
             trace_buf[((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)) * 16 + (j)] = clock64(); \
     } while (0)
 

@@ -71,13 +71,13 @@ cnt = np.bincount([len(v) for v in per_sm.values()])
 print("CTAs per SM histogram:", {i: int(c) for i, c in enumerate(cnt) if c})
 # clock-domain per-tile breakdown for head 0 (events: 4 S ready, 8 S loaded, 12 exps done, 6 P published,
 # 0 PV issued, 2 S issued)
-clk = lambda ev: tr[:, ev, :min(nt, 16)].astype(np.float64)
+clk = lambda ev: tr[:, ev, :min(nt, 15)].astype(np.float64)
 ghz = ((c1 - c0) / np.maximum(t1 - t0, 1)).mean()
 print(f"SM clock from stamps: {ghz:.3f} GHz")
 s_ready, s_load, exp_done, p_pub = clk(4), clk(8), clk(12), clk(6)
 first = (s_ready[:, 0] - c0) / ghz / 1e3
 print(f"entry -> S(0) ready: mean {first.mean():.2f} us  (Q + first K load, S MMA)")
-last = min(nt, 16) - 1
+last = min(nt, 15) - 1
 tail = (c1 - p_pub[:, last]) / ghz / 1e3
 print(f"P(last) -> exit: mean {tail.mean():.2f} us  (last PV, O read, normalise, store)")
 sm_cyc = (exp_done - s_ready)[:, 1:last]
