@@ -7,12 +7,14 @@ TAG=${1:-prof}
 O=gpurun_out/$TAG
 mkdir -p $O
 P='python tools/dit_check.py 4 --no-ref'
-for spec in "gateup:rf_gemm_kernel<\(int\)256, \(int\)3, \(int\)2" "down:rf_gemm_kernel<\(int\)128, \(int\)2, \(int\)2, \(int\)64" \
+for spec in "gateup:rf_gemm_kernel<\(int\)256, \(int\)3, \(int\)2" "down:rf_gemm_kernel<\(int\)128, \(int\)2, \(int\)2, \(int\)32" \
             "oproj:rf_gemm_kernel<\(int\)128, \(int\)2, \(int\)2, \(int\)128" "qkv:rf_gemm_kernel<\(int\)256, \(int\)5, \(int\)2" \
             "xq_xattn:rf_gemm_kernel<\(int\)128, \(int\)6" "attn_self:rf_attn_fa64_kernel" "norm:rf_dit_norm_mod" \
-            "tick_solve:rf_tick_kernel" "decode:rf_decode_tc_kernel"; do
+            "tick_solve:rf_tick_fast_kernel" "decode:rf_decode_tc_kernel" \
+            "proj_wide_c5:rf_gemm_kernel<\(int\)256, \(int\)2, \(int\)2"; do
   n=${spec%%:*}; r=${spec#*:}
-  if [ $n = tick_solve ]; then prog='python tools/toy_ticks.py 40'; elif [ $n = decode ]; then prog="python tools/decode_one.py 1500 1425 1500 4"; else prog=$P; fi
+  if [ $n = tick_solve ]; then prog='python tools/toy_ticks.py 40'; elif [ $n = decode ]; then prog="python tools/decode_one.py 1500 1425 1500 4"
+  elif [ $n = proj_wide_c5 ]; then prog="$P --frames=6000"; else prog=$P; fi
   skip=12; if [ $n = decode ]; then skip=2; fi
   timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
     -k "regex:$r" -s $skip -c 1 -o $O/$n $prog > $O/$n.log 2>&1
