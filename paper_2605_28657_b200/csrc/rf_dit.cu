@@ -335,6 +335,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
     const int64_t pair_min_m = 1024;
     auto plan = [&](GemmPlan *p, const void *A, const void *Bw, int64_t M, int64_t N, int64_t K) {
         if (!rc) rc = gemm_plan(p, A, Bw, M, N, K, K, K, bn_for(N), M >= pair_min_m ? 2 : 1);
+        p->b_static = true;   // every B of the forward is a weight matrix
     };
     auto plan_proj = plan;
     plan(&d->p_in, d->xin, w->w_in, BN, D, d->in_dim);
@@ -376,6 +377,7 @@ extern "C" int rf_dit_create(const rf_dit_config *cfg, const rf_dit_weights *w, 
         plan_proj(&d->p_o[l], d->att, wo + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_qc[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D);
         if (!rc) rc = gemm_plan(&d->p_qcx[l], d->a, wqc + l * d->q_dim * D, BN, d->q_dim, D, D, D, 128, xattn_cg);
+        d->p_qcx[l].b_static = true;
         plan_proj(&d->p_oc[l], d->att, woc + l * D * d->q_dim, BN, D, d->q_dim);
         plan(&d->p_gu[l], d->a, wgu + l * 2 * (int64_t)c.mlp_hidden * D, BN, 2 * (int64_t)c.mlp_hidden, D);
         plan_proj(&d->p_down[l], d->mlp, wdn + l * D * (int64_t)c.mlp_hidden, BN, D, c.mlp_hidden);
@@ -518,6 +520,7 @@ static int proj_build(Dit &d) {
         for (int64_t l = 0; l < L; ++l) {
             GemmPlan &p = d.proj_wide_plans[g][l];
             RF_TRY(gemm_plan(&p, act[g], wts[g] + l * D * kdim[g], BN, D, kdim[g], kdim[g], kdim[g], 256, 2));
+            p.b_static = true;
             RF_TRY(gemm_plan_c(&p, d.h, D));
         }
     }

@@ -175,6 +175,7 @@ int gemm_run(const GemmPlan &plan, int epi, void *out, int64_t ldo, const float 
     gemm::EpiArgs e{out, ldo, gate, gate_ld, rows_per_batch > 0 ? rows_per_batch : 1, alpha, rope, rope_cols,
                     vt ? (__nv_bfloat16 *)vt->ptr : nullptr, vt ? vt->col0 : 0, vt ? vt->heads : 0,
                     vt ? vt->ld : 0, vt ? vt->period : 0, vt ? vt->layer_stride : 0, g_trace};
+    e.b_static = p.b_static ? 1 : 0;
     if (g_trace && g_trace_seq_max > 0)   // each launch (also each captured graph node) its own block
         e.trace = g_trace_seq_next < g_trace_seq_max ? g_trace + kTraceBlock * g_trace_seq_next++ : nullptr;
     if (nf) {

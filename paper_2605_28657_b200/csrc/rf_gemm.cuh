@@ -72,6 +72,9 @@ struct EpiArgs {
     // the attention kernel's maps); query head = n / 128, KV head = head / x_group.
     int x_rpb, x_mtpb, x_batches, x_nk, x_group, x_hkv;
     float x_scale;   // log2(e) / sqrt(head dim)
+    // B is constant across kernels (model weights): the producer may request its first
+    // weight blocks before griddepcontrol.wait
+    int b_static;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -193,7 +196,9 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_wait();     // the previous kernel's outputs (A, the residual stream) are visible
+    // the previous kernel's outputs (A, the residual stream) are visible after pdl_wait; the
+    // producer waits only after requesting the weight blocks of its first tile (below)
+    if (warp != 0) pdl_wait();
     pdl_launch();
     RF_GTRACE(13);
 
@@ -229,6 +234,30 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
             // weights (B) stream through L2 once per forward: evict them first, so the
             // activations the next kernels read stay resident
             const uint64_t pol_w = createpolicy_evict_first();
+            // The weights do not depend on the previous kernel: the first tile's first STAGES
+            // weight blocks are requested before griddepcontrol.wait (a CTA that starts on an SM
+            // the previous grid has left overlaps their DRAM latency with that grid's tail).
+            // Fresh barriers: these stages' first empty waits would pass at once.
+            int pre = 0;
+            {
+                int t, kb0, kb1;
+                Walk w = walk_init();
+                if (epi.b_static && walk_next(w, t, kb0, kb1)) {
+                    const int n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
+                    pre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
+                    for (int s = 0; s < pre; ++s) {
+                        if constexpr (CG == 2) {
+                            if (rank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+                            tma_load_2d_pair_hint(sB + s * C::B_BYTES, &tma_b, mapa_shared(&full[s], 0), (kb0 + s) * BK,
+                                                  n0, pol_w);
+                        } else {
+                            mbar_expect_tx(&full[s], C::STAGE_BYTES);
+                            tma_load_2d_hint(sB + s * C::B_BYTES, &tma_b, &full[s], (kb0 + s) * BK, n0, pol_w);
+                        }
+                    }
+                }
+            }
+            pdl_wait();
             int stage = 0;
             uint32_t phase = 0;
             int it = 0, t, kb0, kb1;
@@ -236,17 +265,18 @@ rf_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant_
                 const int m0 = row0(t), n0 = (t / num_m) * BN + (int)rank * C::BN_LOAD;
                 RF_TRACE(it, 6);
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    const bool early = it == 0 && kb - kb0 < pre;   // B requested before pdl_wait
+                    if (!early) mbar_wait(&empty[stage], phase ^ 1);
                     if constexpr (CG == 2) {
                         // both CTAs' bytes complete on the leader's full barrier
-                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+                        if (rank == 0 && !early) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
                         const uint32_t fb = mapa_shared(&full[stage], 0);
                         tma_load_2d_pair(sA + stage * C::A_BYTES, &tma_a, fb, kb * BK, m0);
-                        tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tma_b, fb, kb * BK, n0, pol_w);
+                        if (!early) tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tma_b, fb, kb * BK, n0, pol_w);
                     } else {
-                        mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+                        if (!early) mbar_expect_tx(&full[stage], C::STAGE_BYTES);
                         tma_load_2d(sA + stage * C::A_BYTES, &tma_a, &full[stage], kb * BK, m0);
-                        tma_load_2d_hint(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0, pol_w);
+                        if (!early) tma_load_2d_hint(sB + stage * C::B_BYTES, &tma_b, &full[stage], kb * BK, n0, pol_w);
                     }
                     if (++stage == STAGES) {
                         stage = 0;

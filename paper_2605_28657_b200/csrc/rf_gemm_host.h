@@ -15,6 +15,7 @@ struct GemmPlan {
     int64_t M, N, K;
     int bn;
     int cg;   // 1: 128 x bn tiles per CTA; 2: 256 x bn tiles per CTA pair (cta_group::2)
+    bool b_static = false;   // B holds weights no kernel writes (see gemm::EpiArgs::b_static)
 };
 
 int make_tmap_bf16_2d(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes,
